@@ -1,0 +1,511 @@
+#!/usr/bin/env python
+"""Benchmark of the speculative-sampling verification step (arXiv 2406.11016).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload c2] [--variant exact|sigmoid] [--no-extra]
+
+One "step" = one verification call over one batch (B x gamma drafted tokens)
+of synthetic logits made by the reference bench recipe (bench.cpp:46-74,
+global batch row b seeded 1 + b).  Metric (BASELINE.json): verified drafted
+tokens/s = N * B * gamma / max-over-ranks(seconds per step), whole job.
+
+* value     device-resident inputs, K steps replayed as one CUDA graph, CUDA
+            events on the launching stream; inputs rotate over R copies whose
+            total exceeds 3x L2 so every step reads HBM.
+* e2e       the same metric through the host C-ABI entry point
+            (ssv_verify_*_host): pinned host logits -> H2D -> kernels -> D2H of
+            every result, synchronized each step.
+* roofline  dominant kernel: algorithmic bytes / its event-timed duration vs
+            MEASURED_PEAKS.json hbm_gbs.
+* cpu_baseline  the reference itself (oracle/_ref, compiled from the reference
+            sources) timed on this host, rank 0 at N=1, bounded sample.
+Multi-GPU: torchrun, one rank per GPU, batch rows sharded with no collective
+on the data path (weak scaling: B rows per GPU).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "verified drafted tokens/sec and achieved HBM GB/s (% of roofline), 1/2/4/8 B200"
+WORKLOADS = {
+    # key: (description, B per GPU, gamma, V, storage)
+    "c1": ("C1 exact verify B=1 gamma=5 V=32000 fp32 (reference CPU workload)", 1, 5, 32000, "f32"),
+    "c2": ("C2 Whisper-shape ASR verify B=8 gamma=5 V=51865 fp32", 8, 5, 51865, "f32"),
+    "c3": ("C3 Llama-2-shape verify B=64 gamma=8 V=32000 fp32", 64, 8, 32000, "f32"),
+    "c3bf16": ("C3 Llama-2-shape verify B=64 gamma=8 V=32000 bf16", 64, 8, 32000, "bf16"),
+    "c4": ("C4 large-vocab verify B=256 gamma=8 V=151936 fp32 (per GPU)", 256, 8, 151936, "f32"),
+    "c4shard": ("C4 large-vocab verify B=32/GPU (256 over 8 GPUs) gamma=8 V=151936 fp32", 32, 8, 151936, "f32"),
+}
+BYTES = {"f32": 4, "bf16": 2, "f64": 8}
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def load_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        p = json.load(open(path))
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def load_traffic(key):
+    path = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    try:
+        return json.load(open(path)).get(key)
+    except Exception:
+        return None
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi-equivalent clocks / throttle reasons via NVML during the timed region."""
+
+    def __init__(self, device_index):
+        self.samples, self.reasons = [], set()
+        self.ok = False
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device_index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception as e:  # pragma: no cover
+            log("clock sampling unavailable:", e)
+        self._stop = threading.Event()
+
+    def _run(self):
+        nv = self.nv
+        names = {
+            "gpu_idle": 0x1, "applications_clocks_setting": 0x2, "sw_power_cap": 0x4, "hw_slowdown": 0x8,
+            "sync_boost": 0x10, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+            "hw_power_brake_slowdown": 0x80, "display_clock_setting": 0x100,
+        }
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for n, bit in names.items():
+                    if r & bit and n != "gpu_idle":
+                        self.reasons.add(n)
+            except Exception:
+                pass
+            time.sleep(0.002)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *exc):
+        if self.ok:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.ok or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": getattr(self, "max_mhz", None), "reasons": sorted(self.reasons),
+                    "samples": 0}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# ----------------------------------------------------------------------------- device arm
+class Workload:
+    def __init__(self, v, key, rank, variant, rotate=True):
+        import torch
+
+        desc, B, gamma, V, storage = WORKLOADS[key]
+        self.key, self.desc, self.B, self.gamma, self.V, self.storage = key, desc, B, gamma, V, storage
+        self.variant = variant
+        self.s = BYTES[storage]
+        tdt = {"f32": torch.float32, "bf16": torch.bfloat16}[storage]
+        zp, zq, ids, u = v.make_bench_inputs(1 + rank * B, B, gamma, V, tdt)
+        torch.cuda.synchronize()
+        self.set_bytes = (zp.numel() + zq.numel()) * self.s
+        l2 = torch.cuda.get_device_properties(torch.cuda.current_device()).L2_cache_size
+        self.l2 = l2
+        R = max(2, math.ceil(3 * l2 / self.set_bytes)) if rotate else 1
+        R = min(R, max(1, int(40e9 // self.set_bytes)))
+        self.R = R
+        self.sets = [(zp, zq, ids, u)] + [(zp.clone(), zq.clone(), ids.clone(), u.clone()) for _ in range(R - 1)]
+        self.outs = None
+
+    def call(self, v, k, out=None):
+        zp, zq, ids, u = self.sets[k % self.R]
+        if self.variant == "exact":
+            return v.verify_exact(zp, zq, ids, u, out=out)
+        return v.verify_sigmoid(zp, zq, ids, u, -1e3, 1e3, out=out)
+
+    def algorithmic_bytes(self, res):
+        """exact s*V*(2*gamma*B + A) + small terms;
+        sigmoid s*V*(A + 2R) + gathers; A = rows that accepted all gamma."""
+        import numpy as np
+
+        acc = np.asarray(res.accepted_len.cpu())
+        A = int((acc == self.gamma).sum())
+        Rr = self.B - A
+        B, g, V, s = self.B, self.gamma, self.V, self.s
+        small = 4 * B * g + 8 * B * (g + 1) + (17 + 8 * g) * B
+        if self.variant == "exact":
+            step = s * V * (2 * g * B + A) + small
+            k1 = s * V * 2 * g * B
+            return step, k1, A
+        step = s * V * (A + 2 * Rr) + 2 * s * B * g + small
+        return step, step, A
+
+
+def capture(v, wl, steps, stream):
+    import torch
+
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(stream):
+        v.set_stream(stream)
+        with torch.cuda.graph(g, stream=stream):
+            for k in range(steps):
+                wl.call(v, k, out=wl.outs[k % wl.R])
+    return g
+
+
+def measure_device(v, wl, K, W, world, sampler=None):
+    """Returns dict(ms_per_step, kernel_ms, launches, result)."""
+    import torch
+
+    stream = torch.cuda.Stream()
+    v.set_stream(stream)
+    # outputs per rotating set; first call also sizes the context scratch
+    wl.outs = [None] * wl.R
+    with torch.cuda.stream(stream):
+        for k in range(wl.R):
+            wl.outs[k] = wl.call(v, k)
+    stream.synchronize()
+    launches_per_step = v.last_launch_count
+    st = int(wl.outs[0].status.item())
+    if st:
+        raise RuntimeError(f"device status {st} on the synthetic inputs")
+    g_warm = capture(v, wl, max(W, 1), stream)
+    g_time = capture(v, wl, K, stream)
+    # kernel timing: an instrumented replica of the timed graph
+    v.profile_enable(K * launches_per_step + 8)
+    g_prof = capture(v, wl, K, stream)
+    v.profile_disable()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+
+    def barrier():
+        if world > 1:
+            import torch.distributed as dist
+
+            dist.barrier()
+
+    with torch.cuda.stream(stream):
+        g_warm.replay()
+        stream.synchronize()
+        barrier()
+        torch.cuda.synchronize()
+        ctx = sampler if sampler is not None else _Null()
+        with ctx:
+            e0.record(stream)
+            g_time.replay()
+            e1.record(stream)
+            stream.synchronize()
+        barrier()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1)
+        g_prof.replay()
+        stream.synchronize()
+    kern = {}
+    for kid, name in ((0, "k_row_stats"), (1, "k_row_pass")):
+        tot, n = v.profile_read(kid)
+        if n:
+            kern[name] = tot / n
+    v.set_stream(None)
+    return {"ms_per_step": ms / K, "kernel_ms": kern, "launches_per_step": launches_per_step,
+            "result": wl.outs[0]}
+
+
+class _Null:
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        pass
+
+
+def measure_e2e(v, wl, K, W):
+    """Host entry point: pinned host inputs -> H2D -> step -> D2H, sync per step."""
+    import numpy as np
+    import torch
+
+    zp, zq, ids, u = wl.sets[0]
+    hz = {}
+    for name, t in (("zp", zp), ("zq", zq)):
+        a = v.host_empty(tuple(t.shape), np.uint16 if wl.storage == "bf16" else np.float32)
+        a[...] = (t.view(torch.int16).cpu().numpy().view(np.uint16) if wl.storage == "bf16" else t.cpu().numpy())
+        hz[name] = a
+    hids = v.host_empty(tuple(ids.shape), np.int32)
+    hids[...] = ids.cpu().numpy()
+    hu = v.host_empty(tuple(u.shape), np.float64)
+    hu[...] = u.cpu().numpy()
+    B, g = wl.B, wl.gamma
+    from paper_2406_11016_b200.ssv import VerifyResult
+
+    out = VerifyResult(v.host_empty((B,), np.int32), v.host_empty((B,), np.int32), v.host_empty((B,), np.uint8),
+                       v.host_empty((B, g), np.float64), v.host_empty((B,), np.float64),
+                       status=v.host_empty((1,), np.uint32))
+    fn = v.verify_exact_host if wl.variant == "exact" else v.verify_sigmoid_host
+    dt = "bfloat16" if wl.storage == "bf16" else None
+    for _ in range(W):
+        fn(hz["zp"], hz["zq"], hids, hu, out=out, dtype=dt)
+    t0 = time.perf_counter()
+    for _ in range(K):
+        fn(hz["zp"], hz["zq"], hids, hu, out=out, dtype=dt)
+    t = (time.perf_counter() - t0) / K
+    h2d = hz["zp"].nbytes + hz["zq"].nbytes + hids.nbytes + hu.nbytes
+    d2h = B * 4 + B * 4 + B + B * g * 8 + B * 8 + 4
+    return t, h2d, d2h, v.last_launch_count
+
+
+# ----------------------------------------------------------------------------- CPU arm
+def cpu_inputs(wl):
+    zp, zq, ids, u = wl.sets[0]
+    return (zp.double().cpu().numpy(), zq.double().cpu().numpy(), ids.cpu().numpy(), u.cpu().numpy())
+
+
+def cpu_time(zp, zq, ids, u, gamma, variant, budget_s, workers):
+    """Time the reference's CPU path (oracle/_ref if built, else the C port) on
+    a bounded row sample.  Returns dict for the JSON line."""
+    import numpy as np
+
+    from oracle.oracle import Oracle, Ref, ref_available
+
+    B = zp.shape[0]
+    if ref_available():
+        ref = Ref()
+        backend = 1 if variant == "exact" else 2
+        # one probe step on one row to size the sample
+        ns, _ = ref.time_backend(backend, zp[:1], zq[:1], ids[:1], u[:1], workers=workers, warmup=0, trials=1)
+        per_row = ns[0] * 1e-9
+        rows = int(max(1, min(B, budget_s / 4 / max(per_row, 1e-9))))
+        trials = int(max(3, min(30, budget_s / max(per_row * rows, 1e-9))))
+        ns, _ = ref.time_backend(backend, zp[:rows], zq[:rows], ids[:rows], u[:rows], workers=workers,
+                                 warmup=1, trials=trials)
+        t = float(np.median(ns)) * 1e-9
+        name = ("pooled materialize_softmax_into + verify_fused" if variant == "exact"
+                else "verify_sigmoid_fused")
+        return {"value": rows * gamma / t, "unit": "tokens/s", "cores": workers, "kind": "reference",
+                "sample": f"{rows} of {B} batch rows, median of {trials} steps, {name} "
+                          f"(WorkerPool({workers}), tile 1024), oracle/_ref compiled from the reference sources"}
+    o = Oracle()
+    rows = 1
+    t0 = time.perf_counter()
+    n = 0
+    while time.perf_counter() - t0 < budget_s / 2 or n < 3:
+        if variant == "exact":
+            o.verify_exact(zp[:rows], zq[:rows], ids[:rows], u[:rows])
+        else:
+            o.verify_sigmoid(zp[:rows], zq[:rows], ids[:rows], u[:rows], -1e3, 1e3)
+        n += 1
+    t = (time.perf_counter() - t0) / n
+    return {"value": rows * gamma / t, "unit": "tokens/s", "cores": 1, "kind": "port",
+            "sample": f"1 of {B} batch rows x {n} steps, oracle/ssv_oracle.c (sequential)"}
+
+
+def run_reference_arm(args):
+    """bench.py --impl reference: the reference's own CPU path, rank 0 only."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import numpy as np
+
+    from oracle.oracle import Oracle, Ref, ref_available
+
+    desc, B, gamma, V, storage = WORKLOADS[args.workload]
+    N = args.gpus
+    o = Oracle()
+    zp, zq, ids, u = o.make_bench_batch(1, B, gamma, V)
+    zp = o.round_f32(zp) if storage == "f32" else o.round_bf16(zp)
+    zq = o.round_f32(zq) if storage == "f32" else o.round_bf16(zq)
+    workers = os.cpu_count() or 1
+    budget = 150.0  # seconds for the whole --steps run
+    if ref_available():
+        ref = Ref()
+        backend = 1 if args.variant == "exact" else 2
+        ns, _ = ref.time_backend(backend, zp[:1], zq[:1], ids[:1], u[:1], workers=workers, warmup=0, trials=1)
+        per_row = ns[0] * 1e-9
+        rows = int(max(1, min(B, budget / (args.steps + args.warmup) / max(per_row, 1e-9))))
+        ns, _ = ref.time_backend(backend, zp[:rows], zq[:rows], ids[:rows], u[:rows], workers=workers,
+                                 warmup=args.warmup, trials=args.steps)
+        kind = "reference"
+        sample = (f"{rows} of {B} batch rows per step, reference "
+                  f"{'pooled softmax + verify_fused' if args.variant == 'exact' else 'verify_sigmoid_fused'} "
+                  f"on WorkerPool({workers})")
+        t = float(np.median(ns)) * 1e-9
+    else:
+        rows, kind, workers = 1, "port", 1
+        times = []
+        for i in range(args.warmup + args.steps):
+            t0 = time.perf_counter()
+            o.verify_exact(zp[:1], zq[:1], ids[:1], u[:1])
+            if i >= args.warmup:
+                times.append(time.perf_counter() - t0)
+        t = statistics.median(times)
+        sample = "1 batch row per step, oracle port (sequential)"
+    value = rows * gamma / t
+    line = {"metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": N, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (make_bench_inputs, bench.cpp:46-74)",
+            "config": {"workload": desc, "variant": args.variant, "B": B, "gamma": gamma, "V": V},
+            "impl": "reference",
+            "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": workers, "kind": kind, "sample": sample},
+            "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------- main
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=2000)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
+    ap.add_argument("--variant", default="exact", choices=["exact", "sigmoid"])
+    ap.add_argument("--no-extra", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        ap.error("--warmup must be >= 3")
+    if args.impl == "reference":
+        return run_reference_arm(args)
+
+    import torch
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2406_11016_b200 import Verifier
+
+    v = Verifier(local)
+    peak, peak_src = load_peaks()
+    wl = Workload(v, args.workload, rank, args.variant)
+    sampler = ClockSampler(local)
+    m = measure_device(v, wl, args.steps, args.warmup, world, sampler)
+    step_bytes, k_bytes, A = wl.algorithmic_bytes(m["result"])
+
+    e2e_t, h2d, d2h, e2e_launches = measure_e2e(v, wl, max(3, min(args.steps, 50)), 3)
+
+    def allmax(x):
+        if world == 1:
+            return x
+        import torch.distributed as dist
+
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    ms = allmax(m["ms_per_step"])
+    e2e_t = allmax(e2e_t)
+    tokens = world * wl.B * wl.gamma
+    dom = "k_row_stats" if args.variant == "exact" else "k_row_pass"
+    kms = m["kernel_ms"].get(dom)
+    achieved = k_bytes / (kms * 1e-3) / 1e9 if kms else None
+    traffic = load_traffic(f"{args.workload}-{args.variant}")
+    line = {
+        "metric": METRIC,
+        "value": tokens / (ms * 1e-3),
+        "unit": "tokens/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": ms,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": wl.storage,
+        "data": "synthetic logits by the reference bench recipe (bench.cpp:46-74), global batch row b seeded 1+b",
+        "config": {
+            "workload": wl.desc, "variant": args.variant, "B_per_gpu": wl.B, "global_batch": world * wl.B,
+            "gamma": wl.gamma, "V": wl.V, "parallelism": f"batch rows sharded over {world} GPU(s), no collective",
+            "l2": f"inputs rotate over {wl.R} copies ({wl.R * wl.set_bytes / 1e6:.0f} MB > 3x L2 "
+                  f"{wl.l2 / 1e6:.0f} MB), every step reads HBM",
+            "timing": "K steps replayed as one CUDA graph, CUDA events on the launching stream, max over ranks",
+        },
+        "gpu_launches": args.steps * m["launches_per_step"],
+        "hbm_gbs_step": step_bytes / (ms * 1e-3) / 1e9,
+        "accepted_all_rows": A,
+        "e2e": {"value": tokens / e2e_t, "unit": "tokens/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                "ms_per_step": e2e_t * 1e3,
+                "path": "ssv_verify_%s_host (C-ABI host entry, pinned host buffers, sync per step)" % args.variant},
+        "roofline": {
+            "bound": "hbm", "kernel": dom,
+            "achieved": achieved, "peak": peak, "unit": "GB/s",
+            "frac": (achieved / peak) if achieved else None,
+            "traffic": traffic.get("dram_bytes_per_launch") if traffic else None,
+            "algorithmic_bytes_per_launch": k_bytes,
+            "kernel_ms": kms, "peak_source": peak_src,
+            "kernels_ms": m["kernel_ms"],
+        },
+        "clocks": sampler.summary(),
+    }
+    if rank == 0 and world == 1 and not args.no_cpu:
+        try:
+            zp, zq, ids, u = cpu_inputs(wl)
+            line["cpu_baseline"] = cpu_time(zp, zq, ids, u, wl.gamma, args.variant, 12.0, os.cpu_count() or 1)
+        except Exception as e:  # the baseline is reported, never required
+            line["cpu_baseline"] = {"value": None, "error": str(e)}
+    if rank == 0 and world == 1 and not args.no_extra:
+        extra = {}
+        for key, variant in (("c2", "sigmoid" if args.variant == "exact" else "exact"), ("c3", "exact"),
+                             ("c3bf16", "exact"), ("c3", "sigmoid"), ("c4", "exact"), ("c4", "sigmoid")):
+            if key == args.workload and variant == args.variant:
+                continue
+            try:
+                w2 = Workload(v, key, 0, variant)
+                m2 = measure_device(v, w2, 200, 5, 1)
+                sb, kb, A2 = w2.algorithmic_bytes(m2["result"])
+                d = "k_row_stats" if variant == "exact" else "k_row_pass"
+                km = m2["kernel_ms"].get(d)
+                extra[f"{key}-{variant}"] = {
+                    "tokens_per_s": w2.B * w2.gamma / (m2["ms_per_step"] * 1e-3),
+                    "ms_per_step": m2["ms_per_step"], "step_gbs": sb / (m2["ms_per_step"] * 1e-3) / 1e9,
+                    "kernel": d, "kernel_ms": km,
+                    "kernel_gbs": kb / (km * 1e-3) / 1e9 if km else None,
+                    "kernel_frac": kb / (km * 1e-3) / 1e9 / peak if km else None,
+                    "kernels_ms": m2["kernel_ms"], "accepted_all_rows": A2, "B": w2.B,
+                }
+                del w2
+                torch.cuda.empty_cache()
+            except Exception as e:
+                extra[f"{key}-{variant}"] = {"error": str(e)}
+        line["extra"] = extra
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,310 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the oracle on the same
+inputs and the same uniforms.  Bar (BASELINE.json north star): accepted
+lengths and tokens identical, any mismatch explained by |u - threshold| < 1e-6;
+tau and residual_denom within 1e-6 absolute (validate.cpp:21-44); p / q /
+residual within 1e-5 relative (+ absolute floor for cancelling residuals)."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+from tests.parity import compare, round_for, to_device
+
+pytestmark = pytest.mark.gpu
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden", "golden_v1.json")
+
+
+def _run(verifier, kind, zp_t, zq_t, ids_t, u_t, alpha=-1e3, beta=1e3, flags=0):
+    if kind == "exact":
+        r = verifier.verify_exact(zp_t, zq_t, ids_t, u_t, flags=flags)
+    elif kind == "sigmoid":
+        r = verifier.verify_sigmoid(zp_t, zq_t, ids_t, u_t, alpha, beta, flags=flags)
+    else:
+        r = verifier.verify_probs(zp_t, zq_t, ids_t, u_t, flags=flags)
+    import torch
+
+    torch.cuda.synchronize()
+    assert int(r.status.item()) == 0, f"device status {int(r.status.item())}"
+    return r
+
+
+def _oracle(oracle, kind, zp, zq, ids, u, alpha=-1e3, beta=1e3):
+    if kind == "exact":
+        return oracle.verify_exact(zp, zq, ids, u)
+    if kind == "sigmoid":
+        return oracle.verify_sigmoid(zp, zq, ids, u, alpha, beta)
+    return oracle.verify_sequential(zp, zq, ids, u)
+
+
+def test_golden_vectors(verifier, oracle):
+    """Every committed golden case (expected outputs of the reference itself)."""
+    from tests.golden.make_golden import rebuild_inputs
+    from oracle.oracle import Result
+
+    g = json.load(open(GOLDEN))
+    mism = 0
+    for case in g["cases"]:
+        zp, zq, ids, u = rebuild_inputs(oracle, case)
+        kind = case["kind"]
+        rnd = case.get("recipe", {}).get("round", "f32" if kind != "probs" else "none")
+        dtype = {"f32": "f32", "bf16": "bf16", "none": "f64"}[rnd] if "recipe" in case else (
+            "f64" if kind == "probs" else "f32")
+        a, b = case.get("alpha", -1e3), case.get("beta", 1e3)
+        r = _run(verifier, kind, *to_device(oracle, zp, zq, ids, u, dtype), a, b)
+        exp = Result(*np.array(ids).shape)
+        for k, v in case["expect"].items():
+            setattr(exp, k, np.array(v, dtype=getattr(exp, k).dtype))
+        mism += compare(exp, r, zp, zq, ids, u, kind, a, b, label=case["id"])
+    assert mism <= 1
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16", "f64"])
+def test_exact_grid(verifier, oracle, dtype):
+    """validate.cpp:221-257-style grid on logits: B in {1,4}, gamma 1..20,
+    V in {7, 257, 50257, 51865}, bonus row on/off."""
+    rng = np.random.default_rng({"f32": 1, "bf16": 2, "f64": 3}[dtype])
+    state = (0xE4AC + len(dtype), 0)
+    mism = 0
+    for i in range(40):
+        B = int(rng.choice([1, 4]))
+        gamma = int(rng.integers(1, 21))
+        V = int(rng.choice([7, 257, 50257, 51865] if i % 3 == 0 else [7, 257, 1000]))
+        bonus = bool(rng.integers(0, 2))
+        (zp, zq, ids, u), state = oracle.make_logit_instance(state, B, gamma, V, bonus, 3.0)
+        zp, zq = round_for(oracle, zp, dtype), round_for(oracle, zq, dtype)
+        o = oracle.verify_exact(zp, zq, ids, u)
+        g = _run(verifier, "exact", *to_device(oracle, zp, zq, ids, u, dtype))
+        mism += compare(o, g, zp, zq, ids, u, "exact", label=f"grid{i}")
+    assert mism <= 1
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_exact_bench_shapes(verifier, oracle, dtype):
+    """bench recipe (bench.cpp:46-74) at C1 (several seeds), C2 and C3 shapes."""
+    mism = 0
+    for seed, B, gamma, V in [(s, 1, 5, 32000) for s in range(1, 17)] + [(1, 8, 5, 51865), (1, 64, 8, 32000)]:
+        zp, zq, ids, u = oracle.make_bench_batch(seed, B, gamma, V)
+        zp, zq = round_for(oracle, zp, dtype), round_for(oracle, zq, dtype)
+        o = oracle.verify_exact(zp, zq, ids, u)
+        g = _run(verifier, "exact", *to_device(oracle, zp, zq, ids, u, dtype))
+        mism += compare(o, g, zp, zq, ids, u, "exact", label=f"bench{seed}-{B}-{V}")
+    assert mism <= 1
+
+
+@pytest.mark.parametrize("scale,mag", [(3.0, 1e3), (800.0, 1e4), (3.0, 1e4), (800.0, 1e3)])
+def test_sigmoid_grid(verifier, oracle, scale, mag):
+    """oracle-sigmoid grid (validate.cpp:259-321), emulate_half = false."""
+    rng = np.random.default_rng(int(scale + mag))
+    state = (0x516 + int(mag), 0)
+    mism = 0
+    for i in range(25):
+        B = int(rng.choice([1, 4]))
+        gamma = int(rng.integers(1, 21))
+        V = int(rng.choice([7, 257, 50257] if i % 3 == 0 else [7, 257, 999]))
+        bonus = bool(rng.integers(0, 2))
+        (zp, zq, ids, u), state = oracle.make_sigmoid_instance(state, B, gamma, V, bonus, scale)
+        zp, zq = oracle.round_f32(zp), oracle.round_f32(zq)
+        o = oracle.verify_sigmoid(zp, zq, ids, u, -mag, mag)
+        g = _run(verifier, "sigmoid", *to_device(oracle, zp, zq, ids, u, "f32"), -mag, mag)
+        mism += compare(o, g, zp, zq, ids, u, "sigmoid", -mag, mag, label=f"sig{i}")
+    assert mism <= 1
+
+
+def test_sigmoid_bench_shape(verifier, oracle):
+    for mag in (1e3, 1e4):
+        zp, zq, ids, u = oracle.make_bench_batch(1, 8, 5, 51865)
+        zp, zq = oracle.round_f32(zp), oracle.round_f32(zq)
+        o = oracle.verify_sigmoid(zp, zq, ids, u, -mag, mag)
+        g = _run(verifier, "sigmoid", *to_device(oracle, zp, zq, ids, u, "f32"), -mag, mag)
+        assert compare(o, g, zp, zq, ids, u, "sigmoid", -mag, mag) == 0
+
+
+def test_probs_grid_f64(verifier, oracle):
+    """Probabilities in (verify_sequential's own API) on fp64 storage."""
+    rng = np.random.default_rng(99)
+    state = (0x0EAC, 0)
+    for i in range(40):
+        B = int(rng.choice([1, 4]))
+        gamma = int(rng.integers(1, 21))
+        V = int(rng.choice([7, 257, 50257] if i % 4 == 0 else [7, 257]))
+        bonus = bool(rng.integers(0, 2))
+        (p, q, ids, u), state = oracle.make_instance(state, B, gamma, V, bonus)
+        o = oracle.verify_sequential(p, q, ids, u)
+        g = _run(verifier, "probs", *to_device(oracle, p, q, ids, u, "f64"))
+        assert compare(o, g, p, q, ids, u, "probs", label=f"probs{i}") == 0
+
+
+def test_degenerate_residual_fallback(verifier, oracle):
+    """Residual mass <= 1e-12 -> sample p, residual_denom 0, resample_used 1
+    (verify_reference.cpp:57-61), in the probability and sigmoid variants."""
+    rng = np.random.default_rng(5)
+    V, gamma, B = 300, 3, 4
+    q = rng.random((B, gamma, V)) + 0.1
+    p = 0.5 * q  # tau = 0.5 everywhere, residual max(0, p - q) = 0
+    ids = rng.integers(0, V, (B, gamma)).astype(np.int32)
+    u = np.full((B, gamma + 1), 0.75)
+    u[:, gamma] = rng.random(B)
+    o = oracle.verify_sequential(p, q, ids, u)
+    assert (o.resample_used == 1).all() and (o.residual_denom == 0).all()
+    g = _run(verifier, "probs", *to_device(oracle, p, q, ids, u, "f64"))
+    assert compare(o, g, p, q, ids, u, "probs") == 0
+    zq = oracle.round_f32(rng.normal(0, 3, (B, gamma, V)))
+    zp = oracle.round_f32(zq - 100.0)
+    o = oracle.verify_sigmoid(zp, zq, ids, u, -1e3, 1e3)
+    assert (o.residual_denom == 0).all()
+    g = _run(verifier, "sigmoid", *to_device(oracle, zp, zq, ids, u, "f32"))
+    assert compare(o, g, zp, zq, ids, u, "sigmoid") == 0
+
+
+def test_edge_shapes(verifier, oracle):
+    """V = 1, gamma = 1; gamma > 32 (multi-warp acceptance scan); B = 300, V = 5."""
+    state = (0xED6E, 0)
+    for B, gamma, V, bonus in [(1, 1, 1, True), (2, 1, 1, False), (1, 40, 64, True), (300, 2, 5, True),
+                               (3, 33, 1001, False)]:
+        (zp, zq, ids, u), state = oracle.make_logit_instance(state, B, gamma, V, bonus, 3.0)
+        zp, zq = oracle.round_f32(zp), oracle.round_f32(zq)
+        o = oracle.verify_exact(zp, zq, ids, u)
+        g = _run(verifier, "exact", *to_device(oracle, zp, zq, ids, u, "f32"))
+        assert compare(o, g, zp, zq, ids, u, "exact", label=f"edge{B}-{gamma}-{V}") == 0
+
+
+def test_misaligned_device_pointers(verifier, oracle):
+    """Rows starting at arbitrary 4-byte offsets (sub-tensor views)."""
+    import torch
+
+    zp, zq, ids, u = oracle.make_bench_batch(3, 2, 4, 32003)
+    zp, zq = oracle.round_f32(zp), oracle.round_f32(zq)
+    o = oracle.verify_exact(zp, zq, ids, u)
+    tzp, tzq, tids, tu = to_device(oracle, zp, zq, ids, u, "f32")
+    bp = torch.empty(tzp.numel() + 1, dtype=torch.float32, device="cuda")
+    bq = torch.empty(tzq.numel() + 3, dtype=torch.float32, device="cuda")
+    bp[1:].copy_(tzp.reshape(-1))
+    bq[3:].copy_(tzq.reshape(-1))
+    g = _run(verifier, "exact", bp[1:].view(tzp.shape), bq[3:].view(tzq.shape), tids, tu)
+    assert compare(o, g, zp, zq, ids, u, "exact") == 0
+
+
+def test_optional_outputs(verifier, oracle):
+    """p, q, residual grids (activation.cpp:20-37; verify_fused.cpp:50)."""
+    from oracle.oracle import Oracle  # noqa: F401
+
+    state = (0x0707, 0)
+    (zp, zq, ids, u), _ = oracle.make_logit_instance(state, 3, 4, 1999, True, 3.0)
+    zp, zq = oracle.round_f32(zp), oracle.round_f32(zq)
+    from paper_2406_11016_b200 import SSV_WANT_P, SSV_WANT_Q, SSV_WANT_RESIDUAL
+
+    flags = SSV_WANT_P | SSV_WANT_Q | SSV_WANT_RESIDUAL
+    g = _run(verifier, "exact", *to_device(oracle, zp, zq, ids, u, "f32"), flags=flags).numpy()
+    P = np.stack([oracle.softmax(r) for r in zp.reshape(-1, zp.shape[-1])]).reshape(zp.shape)
+    Q = np.stack([oracle.softmax(r) for r in zq.reshape(-1, zq.shape[-1])]).reshape(zq.shape)
+    Rz = np.maximum(P[:, :4] - Q, 0)
+    assert np.allclose(g.p, P, rtol=1e-5, atol=1e-12)
+    assert np.allclose(g.q, Q, rtol=1e-5, atol=1e-12)
+    assert np.all(np.abs(g.residual - Rz) <= 1e-5 * Rz + 1e-6 * (P[:, :4] + Q) + 1e-12)
+    # sigmoid grids
+    g = _run(verifier, "sigmoid", *to_device(oracle, zp, zq, ids, u, "f32"), flags=flags).numpy()
+    Ps = 1 / (1 + np.exp(-(zp + 1e3) / 2e3))
+    Qs = 1 / (1 + np.exp(-(zq + 1e3) / 2e3))
+    assert np.allclose(g.p, Ps, rtol=1e-5)
+    assert np.allclose(g.q, Qs, rtol=1e-5)
+    Rs = np.maximum(Ps[:, :4] - Qs, 0)
+    assert np.all(np.abs(g.residual - Rs) <= 1e-5 * Rs + 1e-6 * Ps[:, :4])
+
+
+def test_host_entry_points_and_errors(verifier, oracle):
+    from paper_2406_11016_b200 import SsvInvalidArgument
+
+    zp, zq, ids, u = oracle.make_bench_batch(4, 2, 5, 32000)
+    zp, zq = oracle.round_f32(zp), oracle.round_f32(zq)
+    o = oracle.verify_exact(zp, zq, ids, u)
+    h = verifier.verify_exact_host(zp.astype(np.float32), zq.astype(np.float32), ids, u)
+    assert compare(o, h, zp, zq, ids, u, "exact") == 0
+    bad = ids.copy()
+    bad[1, 2] = 32000
+    with pytest.raises(SsvInvalidArgument, match="out of vocabulary"):
+        verifier.verify_exact_host(zp.astype(np.float32), zq.astype(np.float32), bad, u)
+    badu = u.copy()
+    badu[0, 0] = 1.0
+    with pytest.raises(SsvInvalidArgument, match="uniforms"):
+        verifier.verify_exact_host(zp.astype(np.float32), zq.astype(np.float32), ids, badu)
+    # sigmoid does not range-check uniforms (verify_sigmoid.cpp:13-33, verify_sigmoid_fused)
+    verifier.verify_sigmoid_host(zp.astype(np.float32), zq.astype(np.float32), ids, badu)
+    nan = zq.astype(np.float32)
+    nan[1, 3, 17] = np.nan
+    with pytest.raises(SsvInvalidArgument, match="non-finite"):
+        verifier.verify_exact_host(zp.astype(np.float32), nan, ids, u)
+    ninf = zp.astype(np.float32)
+    ninf[0, 5, 3] = -np.inf
+    with pytest.raises(SsvInvalidArgument, match="non-finite"):
+        verifier.verify_exact_host(ninf, zq.astype(np.float32), ids, u)
+    with pytest.raises(SsvInvalidArgument, match="ScaleBounds"):
+        verifier.verify_sigmoid_host(zp.astype(np.float32), zq.astype(np.float32), ids, u, 1.0, 2.0)
+    with pytest.raises(SsvInvalidArgument, match="gamma"):
+        verifier.verify_exact_host(zp[:, :3].astype(np.float32), zq.astype(np.float32), ids, u)
+    # the context survives errors
+    h = verifier.verify_exact_host(zp.astype(np.float32), zq.astype(np.float32), ids, u)
+    assert compare(o, h, zp, zq, ids, u, "exact") == 0
+
+
+def test_determinism(verifier, oracle):
+    zp, zq, ids, u = oracle.make_bench_batch(9, 16, 8, 51865)
+    zp, zq = oracle.round_f32(zp), oracle.round_f32(zq)
+    t = to_device(oracle, zp, zq, ids, u, "f32")
+    a = _run(verifier, "exact", *t).numpy()
+    for _ in range(3):
+        b = _run(verifier, "exact", *t).numpy()
+        for f in ("accepted_len", "final_token", "tau", "residual_denom", "resample_used"):
+            assert np.array_equal(getattr(a, f), getattr(b, f))
+
+
+def test_sample_softmax(verifier, oracle):
+    import torch
+
+    rng = np.random.default_rng(11)
+    for V in (1, 7, 32000, 51865):
+        z = oracle.round_f32(rng.normal(0, 4, (9, V)))
+        uu = rng.random(9)
+        exp = [oracle.sample_row(oracle.softmax(r), x) for r, x in zip(z, uu)]
+        got = verifier.sample_softmax(torch.from_numpy(z.astype(np.float32)).cuda(), torch.from_numpy(uu).cuda())
+        assert got.cpu().tolist() == exp
+
+
+def test_device_bench_generator(verifier, oracle):
+    """ssv_make_bench_inputs reproduces make_bench_inputs (bench.cpp:46-74)."""
+    import torch
+
+    B, gamma, V = 3, 4, 32000
+    zp, zq, ids, u = oracle.make_bench_batch(5, B, gamma, V)
+    gzp, gzq, gids, gu = verifier.make_bench_inputs(5, B, gamma, V, torch.float32)
+    torch.cuda.synchronize()
+    assert np.mean(gzp.cpu().numpy() == zp.astype(np.float32)) > 0.9999
+    assert np.mean(gzq.cpu().numpy() == zq.astype(np.float32)) > 0.9999
+    assert np.array_equal(gu.cpu().numpy(), u)
+    assert np.mean(gids.cpu().numpy() == ids) >= 0.9
+
+
+def test_full_size_c4_row_subsample(verifier, oracle):
+    """C4 (B=256, gamma=8, V=151936) at full size on the device; the oracle
+    checks a subsample of batch rows (rows are independent)."""
+    import torch
+
+    B, gamma, V = 256, 8, 151936
+    zp_t, zq_t, ids_t, u_t = verifier.make_bench_inputs(1, B, gamma, V, torch.float32)
+    r = _run(verifier, "exact", zp_t, zq_t, ids_t, u_t).numpy()
+    rows = [0, 1, 77, 128, 200, 255]
+    zp = zp_t[rows].double().cpu().numpy()
+    zq = zq_t[rows].double().cpu().numpy()
+    ids = ids_t[rows].cpu().numpy()
+    u = u_t[rows].cpu().numpy()
+    o = oracle.verify_exact(zp, zq, ids, u)
+    from paper_2406_11016_b200.ssv import VerifyResult
+
+    sub = VerifyResult(r.accepted_len[rows], r.final_token[rows], r.resample_used[rows], r.tau[rows],
+                       r.residual_denom[rows])
+    assert compare(o, sub, zp, zq, ids, u, "exact") == 0
+    # size-independent properties over ALL rows
+    assert (r.accepted_len >= 0).all() and (r.accepted_len <= gamma).all()
+    assert ((r.final_token >= 0) & (r.final_token < V)).all()
+    assert (r.resample_used == (r.accepted_len < gamma)).all()
+    assert ((r.tau >= 0) & (r.tau <= 1)).all()
