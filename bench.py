@@ -165,9 +165,8 @@ class Workload:
         small = 4 * B * g + 8 * B * (g + 1) + (17 + 8 * g) * B
         if self.variant == "exact":
             step = s * V * (2 * g * B + A) + small
-            k1 = s * V * 2 * g * B
-            return step, k1, A
-        step = s * V * (A + 2 * Rr) + 2 * s * B * g + small
+        else:
+            step = s * V * (A + 2 * Rr) + 2 * s * B * g + small
         return step, step, A
 
 
@@ -230,11 +229,11 @@ def measure_device(v, wl, K, W, world, sampler=None):
         g_prof.replay()
         stream.synchronize()
     kern = {}
-    for kid, name in ((0, "k_row_stats"), (1, "k_row_pass")):
+    for kid, name in ((0, "k_verify"), (2, "k_materialize")):
         tot, n = v.profile_read(kid)
         if n:
             kern[name] = tot / n
-    v.set_stream(None)
+    v.set_stream(None)  # back to following torch's current stream
     return {"ms_per_step": ms / K, "kernel_ms": kern, "launches_per_step": launches_per_step,
             "result": wl.outs[0]}
 
@@ -427,7 +426,7 @@ def main():
     ms = allmax(m["ms_per_step"])
     e2e_t = allmax(e2e_t)
     tokens = world * wl.B * wl.gamma
-    dom = "k_row_stats" if args.variant == "exact" else "k_row_pass"
+    dom = "k_verify"
     kms = m["kernel_ms"].get(dom)
     achieved = k_bytes / (kms * 1e-3) / 1e9 if kms else None
     traffic = load_traffic(f"{args.workload}-{args.variant}")
@@ -484,7 +483,7 @@ def main():
                 w2 = Workload(v, key, 0, variant)
                 m2 = measure_device(v, w2, 200, 5, 1)
                 sb, kb, A2 = w2.algorithmic_bytes(m2["result"])
-                d = "k_row_stats" if variant == "exact" else "k_row_pass"
+                d = "k_verify"
                 km = m2["kernel_ms"].get(d)
                 extra[f"{key}-{variant}"] = {
                     "tokens_per_s": w2.B * w2.gamma / (m2["ms_per_step"] * 1e-3),

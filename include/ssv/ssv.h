@@ -85,7 +85,9 @@ typedef struct {
 /* ---- context ----------------------------------------------------------------- */
 int ssv_create(int device, ssv_ctx** out);
 void ssv_destroy(ssv_ctx* ctx);
-/* Use a caller-owned cudaStream_t (NULL = the context's own stream). */
+/* Launch on a caller-owned cudaStream_t (NULL = the legacy default stream, as
+ * everywhere in CUDA).  A new context uses its own non-blocking stream, whose
+ * handle ssv_get_stream returns until the first ssv_set_stream. */
 int ssv_set_stream(ssv_ctx* ctx, void* cuda_stream);
 void* ssv_get_stream(const ssv_ctx* ctx);
 const char* ssv_last_error(const ssv_ctx* ctx);
@@ -98,12 +100,19 @@ const char* ssv_version(void);
  * events on the launching stream -- also under stream capture, where the
  * records become graph nodes and are re-recorded on every replay.
  * ssv_profile_read sums the bracketed durations of one kernel id
- * (0 = row_stats, 1 = row_pass, 2 = materialize, 3 = generator) after the
+ * (0 = verify, 2 = materialize, 3 = generator) after the
  * stream has been synchronized. */
 int ssv_profile_enable(ssv_ctx* ctx, int capacity);
 int ssv_profile_disable(ssv_ctx* ctx);
 int ssv_profile_reset(ssv_ctx* ctx);
 int ssv_profile_read(ssv_ctx* ctx, int32_t kernel_id, double* total_ms, int32_t* count);
+
+/* Diagnostics.  capacity > 0 with host_out == NULL attaches a device buffer
+ * of `capacity` globaltimer stamps (ns) that verify launches fill: [2 * grid]
+ * per-CTA start/end, then [4 * B] per batch row decide start/end and locate
+ * start/end.  host_out != NULL copies the buffer out (after a stream sync);
+ * capacity 0 detaches it. */
+int ssv_debug_trace(ssv_ctx* ctx, int capacity, unsigned long long* host_out, int* grid_out);
 
 /* ---- stream-ordered entry points: every pointer is DEVICE memory ----------- */
 /* Exact step, logits in.  Replaces materialize_softmax_into(z_p) and (z_q)

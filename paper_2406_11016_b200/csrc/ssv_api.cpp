@@ -25,8 +25,9 @@ struct ssv_ctx {
     // stream-ordered scratch
     void* scratch = nullptr;
     size_t scratch_bytes = 0;
-    unsigned* counters = nullptr;  // [2 * counters_n], zero between calls
+    unsigned* counters = nullptr;  // [2 + 3 * counters_n]: next, exit, cnt1[n], cnt2[n], flag[n]
     size_t counters_n = 0;
+    unsigned epoch = 0;            // decision-flag tag, one per launch
     uint32_t* status_dev = nullptr;  // default status word
     // host-entry staging
     void* stage = nullptr;
@@ -34,6 +35,8 @@ struct ssv_ctx {
     uint32_t* status_host = nullptr;  // pinned
     ProfileHook prof;
     bool profiling = false;
+    unsigned long long* trace = nullptr;  // diagnostics (ssv_debug_trace)
+    int trace_cap = 0;
     Launch launcher() { return Launch{stream, &launches, profiling ? &prof : nullptr}; }
 };
 
@@ -116,28 +119,31 @@ int ensure_scratch(ssv_ctx* ctx, size_t bytes, size_t counters_n) {
         if (ctx->counters) CK(cudaFree(ctx->counters));
         ctx->counters = nullptr;
         const size_t nn = std::max(counters_n, ctx->counters_n * 2);
-        CK(cudaMalloc(&ctx->counters, 2 * nn * sizeof(unsigned)));
-        CK(cudaMemset(ctx->counters, 0, 2 * nn * sizeof(unsigned)));
+        CK(cudaMalloc(&ctx->counters, (2 + 3 * nn) * sizeof(unsigned)));
+        CK(cudaMemset(ctx->counters, 0, (2 + 3 * nn) * sizeof(unsigned)));
         ctx->counters_n = nn;
+        ctx->epoch = 0;
     }
     return SSV_OK;
 }
 
 struct Layout {
-    size_t part, rowstat, dec, gpart, extra, total;
+    size_t part, rowstat, dec, gpart, gat, extra, total;
 };
 
 Layout plan_scratch(const StepParams& P, size_t extra_bytes) {
     Layout L;
     size_t off = 0;
     L.part = off;
-    off = align_up(off + (size_t)P.B * P.NR * std::max(P.K, 1) * sizeof(double2));
+    off = align_up(off + (size_t)P.B * P.NR * std::max(P.RPR, 1) * sizeof(double2));
     L.rowstat = off;
     off = align_up(off + (size_t)P.B * std::max(P.NR, 1) * sizeof(double2));
     L.dec = off;
     off = align_up(off + (size_t)P.B * sizeof(Decision));
     L.gpart = off;
     off = align_up(off + (size_t)P.B * P.NG * sizeof(double2));
+    L.gat = off;
+    off = align_up(off + (size_t)P.B * std::max(P.NR, 1) * sizeof(double));
     L.extra = off;
     off = align_up(off + extra_bytes);
     L.total = off;
@@ -150,8 +156,14 @@ void bind_scratch(ssv_ctx* ctx, StepParams& P, const Layout& L) {
     P.rowstat = reinterpret_cast<double2*>(s + L.rowstat);
     P.dec = reinterpret_cast<Decision*>(s + L.dec);
     P.gpart = reinterpret_cast<double2*>(s + L.gpart);
-    P.cnt1 = ctx->counters;
-    P.cnt2 = ctx->counters + ctx->counters_n;
+    P.gat = reinterpret_cast<double*>(s + L.gat);
+    P.next = ctx->counters;
+    P.exit_cnt = ctx->counters + 1;
+    P.cnt1 = ctx->counters + 2;
+    P.cnt2 = P.cnt1 + ctx->counters_n;
+    P.flag = P.cnt2 + ctx->counters_n;
+    P.epoch = ++ctx->epoch;
+    if (P.epoch == 0) P.epoch = ++ctx->epoch;  // flags start at 0: never reuse it
 }
 
 int run_device(ssv_ctx* ctx, int variant, const ssv_verify_args* a, ssv_verify_out* o) {
@@ -169,12 +181,10 @@ int run_device(ssv_ctx* ctx, int variant, const ssv_verify_args* a, ssv_verify_o
     P.PS = a->p_steps;
     const bool want_p = a->flags & SSV_WANT_P;
     P.NR = 2 * P.G + ((want_p && P.PS == P.G + 1) ? 1 : 0);
-    P.NG = (P.V + kGranule - 1) / kGranule;
     P.alpha = a->alpha;
     P.width = a->beta - a->alpha;
     P.check_uniforms = variant != V_SIGMOID;
-    P.K = variant == V_EXACT ? stats_chunks(a->dtype, P) : 0;
-    if (variant != V_EXACT) P.NR = 0;
+    plan_geometry(a->dtype, variant, P);
     const Layout L = plan_scratch(P, 0);
     rc = ensure_scratch(ctx, L.total, (size_t)P.B);
     if (rc) return rc;
@@ -185,6 +195,7 @@ int run_device(ssv_ctx* ctx, int variant, const ssv_verify_args* a, ssv_verify_o
     P.tau = o->tau;
     P.rden = o->residual_denom;
     P.status = o->status ? o->status : ctx->status_dev;
+    P.trace = (ctx->trace && 3 * verify_grid(P) + 4 * P.B <= ctx->trace_cap) ? ctx->trace : nullptr;
     ctx->launches = 0;
     launch_verify(a->dtype, variant, P, want_p ? o->p : nullptr, (a->flags & SSV_WANT_Q) ? o->q : nullptr,
                   (a->flags & SSV_WANT_RESIDUAL) ? o->residual : nullptr, ctx->launcher());
@@ -344,7 +355,7 @@ void ssv_destroy(ssv_ctx* ctx) {
 
 int ssv_set_stream(ssv_ctx* ctx, void* stream) {
     if (!ctx) return SSV_EINVAL;
-    ctx->stream = stream ? static_cast<cudaStream_t>(stream) : ctx->own;
+    ctx->stream = static_cast<cudaStream_t>(stream);  // NULL: the legacy default stream, as in CUDA
     return SSV_OK;
 }
 
@@ -404,6 +415,27 @@ int ssv_profile_read(ssv_ctx* ctx, int32_t kernel_id, double* total_ms, int32_t*
     return SSV_OK;
 }
 
+int ssv_debug_trace(ssv_ctx* ctx, int capacity, unsigned long long* host_out, int* grid_out) {
+    if (!ctx) return SSV_EINVAL;
+    CK(cudaSetDevice(ctx->device));
+    if (host_out) {
+        if (!ctx->trace) return fail(ctx, SSV_EINVAL, "ssv_debug_trace: tracing not enabled");
+        CK(cudaStreamSynchronize(ctx->stream));
+        CK(cudaMemcpy(host_out, ctx->trace, (size_t)ctx->trace_cap * 8, cudaMemcpyDeviceToHost));
+        return SSV_OK;
+    }
+    if (ctx->trace) CK(cudaFree(ctx->trace));
+    ctx->trace = nullptr;
+    ctx->trace_cap = 0;
+    if (capacity > 0) {
+        CK(cudaMalloc(&ctx->trace, (size_t)capacity * 8));
+        CK(cudaMemset(ctx->trace, 0, (size_t)capacity * 8));
+        ctx->trace_cap = capacity;
+    }
+    (void)grid_out;
+    return SSV_OK;
+}
+
 int ssv_verify_exact(ssv_ctx* ctx, const ssv_verify_args* a, ssv_verify_out* o) {
     return run_device(ctx, V_EXACT, a, o);
 }
@@ -448,13 +480,14 @@ int ssv_sample_softmax(ssv_ctx* ctx, int32_t dtype, const void* logits, int32_t 
     P.G = 0;
     P.PS = 1;
     P.V = V;
-    P.NG = (V + kGranule - 1) / kGranule;
     P.sample_mode = 1;
+    plan_geometry(dtype, ACT_SOFTMAX, P);
     const Layout L = plan_scratch(P, 0);
     int rc = ensure_scratch(ctx, L.total, (size_t)rows);
     if (rc) return rc;
     bind_scratch(ctx, P, L);
     P.fin = tokens_out;
+    P.trace = (ctx->trace && 3 * verify_grid(P) + 4 * P.B <= ctx->trace_cap) ? ctx->trace : nullptr;
     P.status = status ? status : ctx->status_dev;
     ctx->launches = 0;
     launch_sample_softmax(dtype, P, ctx->launcher());
@@ -473,8 +506,11 @@ int ssv_make_bench_inputs(ssv_ctx* ctx, uint64_t seed, int32_t B, int32_t gamma,
     // draft-draw uniforms live past the sampler's scratch
     StepParams P{};
     P.B = B * gamma;
+    P.G = 0;
+    P.PS = 1;
     P.V = V;
-    P.NG = (V + kGranule - 1) / kGranule;
+    P.sample_mode = 1;
+    plan_geometry(dtype, ACT_SOFTMAX, P);
     const Layout L = plan_scratch(P, (size_t)B * gamma * sizeof(double));
     int rc = ensure_scratch(ctx, L.total, (size_t)B * gamma);
     if (rc) return rc;

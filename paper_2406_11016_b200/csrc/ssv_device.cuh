@@ -77,6 +77,12 @@ __device__ __forceinline__ float load_elem(const __nv_bfloat16* p) {
 }
 __device__ __forceinline__ double load_elem(const double* p) { return __ldg(p); }
 
+__device__ __forceinline__ float load_smem_elem(const float* p) { return *p; }
+__device__ __forceinline__ float load_smem_elem(const __nv_bfloat16* p) {
+    return __uint_as_float(((uint32_t)*reinterpret_cast<const unsigned short*>(p)) << 16);
+}
+__device__ __forceinline__ double load_smem_elem(const double* p) { return *p; }
+
 // Exact (fp64) value of a stored element.
 template <typename T>
 __device__ __forceinline__ double load_exact(const T* p) {
@@ -107,13 +113,11 @@ __device__ __forceinline__ double sigmoid_scaled_d(double z, double alpha, doubl
     return stable_sigmoid_d((z - alpha) / width);
 }
 
-// Streaming-path sigmoid pieces (fp32 or fp64 `acc`).
-__device__ __forceinline__ float exp_neg(float t) {  // e^-t
-    float r;
-    const float a = -t * 1.4426950408889634f;
-    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(a));
-    return r;
-}
+// Streaming-path sigmoid pieces (fp32 or fp64 `acc`).  The sigmoid variant
+// touches only the rows a batch row still needs, so it affords the accurate
+// (<= 2 ulp, unbiased) expf: its masses are sums of ~V values near 0.5-1 whose
+// rounding must not accumulate a bias (residual_denom parity).
+__device__ __forceinline__ float exp_neg(float t) { return expf(-t); }
 __device__ __forceinline__ double exp_neg(double t) { return exp(-t); }
 __device__ __forceinline__ float expm1_acc(float x) { return expm1f(x); }
 __device__ __forceinline__ double expm1_acc(double x) { return expm1(x); }

@@ -1,32 +1,87 @@
 // ssv_kernels.cu -- sm_100a kernels of the speculative-sampling verification step.
 //
-// Path (DESIGN.md has the full derivation):
-//   K1 k_row_stats   exact variant only.  One CTA per (row, 8K-element chunk) of
-//                    the 2*gamma drafted rows (+ the bonus row when p is
-//                    materialized): 128-bit streaming loads into registers, CTA
-//                    max, fp32 ex2 sums with fp64 carries -> chunk partial
-//                    (m, s).  The LAST CTA of each batch row (completion counter)
-//                    folds the partials into row statistics, evaluates tau at
-//                    every drafted position in fp64, runs the first-rejection
-//                    scan and records what the batch row still needs.
-//   K2 k_row_pass    every variant.  One warp per 512-element granule of the
-//                    ONE row (bonus) or row PAIR (rejected position) a batch row
-//                    still needs; granule masses of max(0, p - q) (or of p) with
-//                    fp64 carries.  The LAST CTA of each batch row does the
-//                    inverse CDF: granule prefix in fp64, then an fp64 element
-//                    scan inside the selected granule -- dist.cpp:122-137
-//                    semantics including the last-positive fallback.  For the
-//                    sigmoid and probability variants K2 is the whole step: its
-//                    CTAs evaluate tau from the B*gamma gathered logits
-//                    themselves (no row reductions).
-//   K3 k_materialize optional p / q / residual grids.
-//   generator / sampler kernels for the callers either side of the path.
+// k_verify<T, ACT> is the whole step in ONE persistent, warp-specialized
+// launch (DESIGN.md has the derivation and the roofline):
+//
+//   producer warp   claims work items in order from a global counter and
+//                   streams their bytes into a kStages-deep ring of shared-
+//                   memory stages with TMA bulk copies (cp.async.bulk, 16-byte
+//                   aligned supersets of misaligned rows) completing on mbarriers.
+//   consumer warps  (8) drain the ring:
+//     A-item  (exact only) one chunk of one drafted p/q row: CTA max, fp32 ex2
+//             sums with fp64 carries -> chunk partial (m, s); the logit at the
+//             drafted token is picked out of the stage.  The consumer group
+//             that completes batch row b's LAST A-item folds the partials into
+//             row statistics, evaluates tau at every drafted position in fp64,
+//             runs the first-rejection scan and publishes the decision
+//             (release flag, tagged with the launch epoch).
+//     D-item  (sigmoid / probabilities) the same decision from the B*gamma
+//             gathered logits alone -- no row reductions (paper section 3.2.2).
+//     B-item  one slice of the ONE row (bonus) or row PAIR (rejected position)
+//             batch row b still needs; the producer waits for b's decision
+//             before fetching it.  Each consumer warp reduces one granule to
+//             its residual mass max(0, p - q) (or p mass / (m, s) for the bonus
+//             row).  B-items of b are ordered after the A-items of b + lag, so
+//             the rejected pair is re-read from L2, not HBM.
+//             The group completing b's LAST B-item runs the inverse CDF: fp64
+//             granule prefix from SMEM, then an exact fp64 scan inside the
+//             selected granule (dist.cpp:122-137, incl. its fallbacks).
+//
+// Every reduction has a fixed topology, so results are bit-identical run to
+// run.  k_materialize (optional p / q / residual grids) and the synthetic-input
+// generator follow.
+#include <algorithm>
 #include <type_traits>
 
 #include "ssv_launch.h"
 #include "ssv_device.cuh"
+#include "ssv_pipe.cuh"
 
 namespace ssv {
+
+constexpr int kCons = 256;                 // consumer threads (8 warps)
+constexpr int kConsWarps = kCons / 32;
+constexpr int kBlock = kCons + 32;         // + one producer warp
+
+// Work-item phases of one batch row, in dependency order.
+enum ItemType : int { IT_A = 0, IT_D = 1, IT_B = 2, IT_L = 3, IT_STOP = 4 };
+constexpr int kMaxRowsSmem = 96;  // row statistics a decide keeps in SMEM (gamma <= 47)
+
+constexpr int kMaxRunA = 64;  // chunks per A-run (row-statistics run)
+constexpr int kMaxRunB = 8;   // slices per B-run (residual / bonus run)
+constexpr int kCtx = 8;       // run contexts (runs in flight per CTA; see RunInfo)
+
+// Work-item description handed from producer to consumers.  A- and B-items
+// are RUNS of consecutive chunks of one row; a run is streamed one 16 KB chunk
+// per ring stage.
+struct Item {
+    int type, b;
+    int r, q;            // A: stat row, run index within the row; B: run index
+    int mode, row;       // B / L: decision
+    double Mp, Sp, Mq, Sq;
+};
+
+// One ring slot (16 bytes for A/B chunks; D/L items also carry the decision).
+struct Slot {
+    int type, ctx, pos, b;
+    int mode, row, pad0, pad1;
+    double Mp, Sp, Mq, Sq;
+};
+
+// Per-run constants (written once by the producer before the run's first
+// chunk is published) and the consumers' fold state.  kCtx contexts: consumer
+// warps can be at most kStages chunks apart (a stage is refilled only after
+// all 8 warps released it), so a context is free again long before the
+// producer reuses it kCtx runs later.
+struct RunInfo {
+    int type, b, r, q, len, k0;  // k0: first chunk (A) / slice (B) of the run
+    int mode, row, shift_p, shift_q;
+    double Mp, Sp, Mq, Sq;
+    double2 wpart[kConsWarps];   // A: warp partials (max, sum) of the run
+    double wmin[kConsWarps];
+    double2 gpart[kMaxRunB * kConsWarps];  // B: granule partials of the run
+    unsigned cnt;                // warps done with the run
+};
 
 // ---------------------------------------------------------------------------
 // Row addressing.  Stat rows of batch row b: r < G -> p row r, G <= r < 2G ->
@@ -48,162 +103,366 @@ __device__ __forceinline__ const T* stat_row(const StepParams& P, int b, int r) 
 
 __device__ __forceinline__ void flag(const StepParams& P, uint32_t bits) { atomicOr(P.status, bits); }
 
+__device__ __forceinline__ unsigned long long gtime() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+// Diagnostics: phase timestamps (ns) when a trace buffer is attached.
+__device__ __forceinline__ void trace(const StepParams& P, int idx) {
+    if (P.trace) P.trace[idx] = gtime();
+}
+
 __device__ __forceinline__ double ratio_clamped(double p, double q) {  // dist.cpp:104-112
     if (q <= kZeroEps) return p > kZeroEps ? 1.0 : 0.0;
     return fmin(1.0, p / q);
 }
 
+// ---- consumer-group collectives (named barrier 1, 256 threads) -------------
+template <typename V, typename Op>
+__device__ __forceinline__ V creduce(V v, V* sm, Op op) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = op(v, __shfl_xor_sync(kFull, v, o));
+    cbar<kCons>();
+    if (lane == 0) sm[warp] = v;
+    cbar<kCons>();
+    V r = sm[0];
+#pragma unroll
+    for (int w = 1; w < kConsWarps; ++w) r = op(r, sm[w]);
+    return r;
+}
+
+__device__ __forceinline__ double cscan_incl(double v, double* sm, double& total) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const double incl = warp_scan_incl(v);
+    cbar<kCons>();
+    if (lane == 31) sm[warp] = incl;
+    cbar<kCons>();
+    double off = 0.0, tot = 0.0;
+#pragma unroll
+    for (int w = 0; w < kConsWarps; ++w) {
+        if (w < warp) off += sm[w];
+        tot += sm[w];
+    }
+    total = tot;
+    return off + incl;
+}
+
+template <typename T>
+__device__ __forceinline__ typename Elem<T>::acc lds_elem(const uint8_t* base, int i) {
+    return (typename Elem<T>::acc)load_smem_elem(reinterpret_cast<const T*>(base) + i);
+}
+
 // ---------------------------------------------------------------------------
-// Register tile of one warp over [lo, hi) of one row: NV 16-byte vectors per
-// lane plus at most one peeled scalar (head to the first 16-byte boundary,
-// lanes 0..; tail, lanes 16..).
-template <typename T, int NV>
-struct WarpTile {
-    using A = typename Elem<T>::acc;
-    static constexpr int VEC = Elem<T>::VEC;
-    uint4 v[NV];
-    int nvec;
-    A xs;
-    bool has_x;
-
-    __device__ __forceinline__ void load(const T* row, int lo, int hi) {
-        const int lane = threadIdx.x & 31;
-        const Span16<T> s = split16(row, lo, hi);
-        nvec = s.nvec;
-        const T* vb = row + s.vec_begin;
+// Work-item order.  Segment t holds, in order, the A-items of batch row t,
+// the decide item of t - off[1], the B-items of t - off[2] and the locate item
+// of t - off[3] (each only if that row exists).  Items only ever wait on items
+// with a smaller index -- claimed earlier by a running CTA -- so the schedule
+// cannot deadlock, and the lags keep the waits short and the rejected pair of
+// row b L2-resident when its B-items stream it again.
+__device__ __forceinline__ int seg_size(const StepParams& P, int t) {
+    int n = 0;
 #pragma unroll
-        for (int j = 0; j < NV; ++j) {
-            const int idx = j * 32 + lane;
-            if (idx < nvec) v[j] = ldg_stream(vb + (size_t)idx * VEC);
-        }
-        has_x = false;
-        const int nh = s.head_end - lo, nt = hi - s.tail_begin;
-        if (lane < nh) {
-            xs = load_elem(row + lo + lane);
-            has_x = true;
-        } else if (lane >= 16 && lane - 16 < nt) {
-            xs = load_elem(row + s.tail_begin + (lane - 16));
-            has_x = true;
-        }
+    for (int p = 0; p < 4; ++p) {
+        const int b = t - P.off[p];
+        if (b >= 0 && b < P.B) n += P.nph[p];
     }
+    return n;
+}
 
-    __device__ __forceinline__ void minmax(A& mx, A& mn) const {
-        const int lane = threadIdx.x & 31;
-#pragma unroll
-        for (int j = 0; j < NV; ++j) {
-            if (j * 32 + lane < nvec) {
-                A x[VEC];
-                unpack(v[j], x);
-#pragma unroll
-                for (int e = 0; e < VEC; ++e) {
-                    mx = fmax(mx, x[e]);
-                    mn = fmin(mn, x[e]);
-                }
-            }
-        }
-        if (has_x) {
-            mx = fmax(mx, xs);
-            mn = fmin(mn, xs);
-        }
-    }
-
-    // sum of e^(x - m): fp32 within a 16-byte vector, fp64 across vectors.
-    __device__ __forceinline__ double sum_exp(A m) const {
-        const int lane = threadIdx.x & 31;
-        double s = 0.0;
-#pragma unroll
-        for (int j = 0; j < NV; ++j) {
-            if (j * 32 + lane < nvec) {
-                A x[VEC];
-                unpack(v[j], x);
-                A t = 0;
-#pragma unroll
-                for (int e = 0; e < VEC; ++e) t += exp_rel(x[e], m);
-                s += (double)t;
-            }
-        }
-        if (has_x) s += (double)exp_rel(xs, m);
-        return s;
-    }
-
-    template <typename F>
-    __device__ __forceinline__ double sum_map(F f) const {
-        const int lane = threadIdx.x & 31;
-        double s = 0.0;
-#pragma unroll
-        for (int j = 0; j < NV; ++j) {
-            if (j * 32 + lane < nvec) {
-                A x[VEC];
-                unpack(v[j], x);
-                A t = 0;
-#pragma unroll
-                for (int e = 0; e < VEC; ++e) t += f(x[e]);
-                s += (double)t;
-            }
-        }
-        if (has_x) s += (double)f(xs);
-        return s;
-    }
+// Position of an item: segment t, phase p, index a within the phase.
+struct Cursor {
+    int t, p, a;
 };
 
-// ---------------------------------------------------------------------------
-// K1 epilogue: the last CTA of batch row b.  Row statistics from the chunk
-// partials (fixed order, fp64), tau at every drafted position (fp64, from the
-// gathered logits -- activation.cpp:20-27 + verify_reference.cpp:87-92),
-// first rejection (verify_reference.cpp:93-96, inclusive u <= tau).
+__device__ __forceinline__ bool phase_active(const StepParams& P, int t, int p) {
+    const int b = t - P.off[p];
+    return P.nph[p] > 0 && b >= 0 && b < P.B;
+}
+
+// First active phase of segment t at or after phase p (p may be 4: next segment).
+__device__ __forceinline__ void settle(const StepParams& P, Cursor& c) {
+    const int tend = P.B + P.off[3];
+    while (c.t < tend) {
+        while (c.p < 4 && !phase_active(P, c.t, c.p)) ++c.p;
+        if (c.p < 4) return;
+        ++c.t;
+        c.p = 0;
+        c.a = 0;
+    }
+}
+
+__device__ __forceinline__ Cursor decode_cursor(const StepParams& P, unsigned i) {
+    Cursor c{P.B + P.off[3], 0, 0};  // past the end
+    if (i >= P.n_items) return c;
+    unsigned cum = 0;
+    int o = 0;
+    for (int q = 0; q + 1 < P.nbp; ++q) {
+        const int x = P.bp[q], y = P.bp[q + 1];
+        const int sz = seg_size(P, x);
+        const unsigned cnt = (unsigned)(y - x) * (unsigned)sz;
+        if (sz > 0 && i < cum + cnt) {
+            c.t = x + (int)((i - cum) / (unsigned)sz);
+            o = (int)((i - cum) % (unsigned)sz);
+            break;
+        }
+        cum += cnt;
+    }
+    c.p = 0;
+    c.a = 0;
+    for (int p = 0; p < 4; ++p) {
+        if (!phase_active(P, c.t, p)) continue;
+        if (o < P.nph[p]) {
+            c.p = p;
+            c.a = o;
+            return c;
+        }
+        o -= P.nph[p];
+    }
+    return c;
+}
+
+__device__ __forceinline__ void advance(const StepParams& P, Cursor& c) {
+    if (++c.a < P.nph[c.p]) return;
+    c.a = 0;
+    ++c.p;
+    settle(P, c);
+}
+
+__device__ __forceinline__ void cursor_item(const StepParams& P, const Cursor& c, Item& it) {
+    it.type = IT_STOP;
+    if (c.t >= P.B + P.off[3]) return;
+    it.type = c.p;
+    it.b = c.t - P.off[c.p];
+    if (c.p == IT_A) {
+        it.r = c.a / P.RPR;
+        it.q = c.a - it.r * P.RPR;
+    } else {
+        it.q = c.a;
+    }
+}
+
+// Bulk-copy the 16-byte-aligned superset of [lo, hi) of `row` into dst;
+// returns the copied bytes and the element shift of `lo` inside it.
 template <typename T>
-__device__ void decide_softmax(const StepParams& P, int b) {
+__device__ __forceinline__ uint32_t stage_range(const T* row, int lo, int hi, uint8_t* dst, uint64_t* bar,
+                                                int& shift) {
+    const uintptr_t a0 = reinterpret_cast<uintptr_t>(row + lo);
+    const uintptr_t a1 = reinterpret_cast<uintptr_t>(row + hi);
+    const uintptr_t s0 = a0 & ~uintptr_t(15), s1 = (a1 + 15) & ~uintptr_t(15);
+    shift = (int)((a0 - s0) / sizeof(T));
+    const uint32_t bytes = (uint32_t)(s1 - s0);
+    bulk_g2s(dst, reinterpret_cast<const void*>(s0), bytes, bar);
+    return bytes;
+}
+
+template <typename T>
+__device__ __forceinline__ uint32_t staged_bytes(const T* row, int lo, int hi) {
+    const uintptr_t a0 = reinterpret_cast<uintptr_t>(row + lo);
+    const uintptr_t a1 = reinterpret_cast<uintptr_t>(row + hi);
+    return (uint32_t)(((a1 + 15) & ~uintptr_t(15)) - (a0 & ~uintptr_t(15)));
+}
+
+// ---------------------------------------------------------------------------
+// Producer: lane 0 of the last warp.  Claims kClaim items per atomic, waits
+// for an item's dependencies (acquire loads of the completion counters and the
+// decision flag), then fills the next ring stage: TMA bulk copies for A- and
+// B-items, a bare arrive for decide / locate items.
+__device__ __forceinline__ void wait_eq(const unsigned* p, unsigned v) {
+    while (ld_acquire(p) != v) __nanosleep(32);
+}
+
+__device__ __forceinline__ bool load_decision(const StepParams& P, Item& it) {
+    if (P.sample_mode) {
+        it.mode = MODE_BONUS;
+        it.row = 0;
+        it.Mp = it.Mq = 0.0;
+        it.Sp = it.Sq = 1.0;
+        return true;
+    }
+    wait_eq(&P.flag[it.b], P.epoch);
+    const Decision* d = &P.dec[it.b];
+    it.mode = __ldcg(&d->mode);
+    if (it.mode == MODE_NONE) return false;
+    it.row = __ldcg(&d->row);
+    it.Mp = __ldcg(&d->Mp);
+    it.Sp = __ldcg(&d->Sp);
+    it.Mq = __ldcg(&d->Mq);
+    it.Sq = __ldcg(&d->Sq);
+    return true;
+}
+
+template <typename T, int ACT>
+__device__ void producer(const StepParams& P, uint8_t* stages, uint64_t* full, uint64_t* empty, Slot* slots,
+                         RunInfo* runs) {
+    constexpr int CA = kStageBytes / (int)sizeof(T);
+    unsigned cur = atomicAdd(P.next, 1u);
+    unsigned nxt = atomicAdd(P.next, 1u);  // next item, claimed one ahead
+    if (P.trace) P.trace[2 * gridDim.x + 4 * P.B + blockIdx.x] = cur;
+    unsigned n = 0, runseq = 0;
+    auto stage = [&](unsigned& sidx) -> uint8_t* {
+        const unsigned s = n % kStages, ph = (n / kStages) & 1u;
+        mbar_wait(&empty[s], ph ^ 1u);
+        sidx = s;
+        return stages + (size_t)s * kStageStride;
+    };
+    for (;;) {
+        Item it;
+        cursor_item(P, decode_cursor(P, cur), it);
+        cur = nxt;
+        nxt = atomicAdd(P.next, 1u);
+        if (it.type == IT_D) {
+            if (ACT == ACT_SOFTMAX && !P.sample_mode) wait_eq(&P.cnt1[it.b], (unsigned)P.nph[IT_A]);
+        } else if (it.type == IT_B) {
+            if (!load_decision(P, it)) continue;
+        } else if (it.type == IT_L) {
+            if (!load_decision(P, it)) continue;
+            wait_eq(&P.cnt2[it.b], (unsigned)P.nph[IT_B]);
+        }
+        if (it.type == IT_A || it.type == IT_B) {
+            const int c = (int)(runseq++ % kCtx);
+            RunInfo& ri = runs[c];
+            const T* pr;
+            const T* qr = nullptr;
+            int k0, k1, step;
+            if (it.type == IT_A) {
+                pr = stat_row<T>(P, it.b, it.r);
+                k0 = it.q * P.runA;
+                k1 = min(k0 + P.runA, P.K);
+                step = CA;
+            } else {
+                pr = p_row<T>(P, it.b, it.row);
+                if (it.mode == MODE_REJECT) qr = q_row<T>(P, it.b, it.row);
+                k0 = it.q * P.runB;
+                k1 = min(k0 + P.runB, P.nBi);
+                step = P.CB;
+            }
+            // chunk starts are 16 KB / 8 KB apart: the misalignment is constant per row
+            ri.type = it.type;
+            ri.b = it.b;
+            ri.r = it.r;
+            ri.q = it.q;
+            ri.len = k1 - k0;
+            ri.k0 = k0;
+            ri.mode = it.mode;
+            ri.row = it.row;
+            ri.Mp = it.Mp;
+            ri.Sp = it.Sp;
+            ri.Mq = it.Mq;
+            ri.Sq = it.Sq;
+            ri.shift_p = (int)((reinterpret_cast<uintptr_t>(pr + (size_t)k0 * step) & 15) / sizeof(T));
+            ri.shift_q = qr ? (int)((reinterpret_cast<uintptr_t>(qr + (size_t)k0 * step) & 15) / sizeof(T)) : 0;
+            for (int k = k0; k < k1; ++k) {
+                unsigned s;
+                uint8_t* st = stage(s);
+                const int lo = k * step, hi = min(lo + step, P.V);
+                uint32_t bytes = staged_bytes(pr, lo, hi);
+                if (qr) bytes += staged_bytes(qr, lo, hi);
+                slots[s].type = it.type;
+                slots[s].ctx = c;
+                slots[s].pos = k - k0;
+                slots[s].b = it.b;
+                mbar_arrive_expect_tx(&full[s], bytes);  // publishes slot + run info (release)
+                int sh;
+                stage_range(pr, lo, hi, st, &full[s], sh);
+                if (qr) stage_range(qr, lo, hi, st + kHalfStride, &full[s], sh);
+                ++n;
+            }
+        } else {
+            unsigned s;
+            stage(s);
+            Slot sl;
+            sl.type = it.type;
+            sl.ctx = -1;
+            sl.pos = 0;
+            sl.b = it.b;
+            sl.mode = it.mode;
+            sl.row = it.row;
+            sl.Mp = it.Mp;
+            sl.Sp = it.Sp;
+            sl.Mq = it.Mq;
+            sl.Sq = it.Sq;
+            slots[s] = sl;
+            mbar_arrive(&full[s]);
+            ++n;
+            if (it.type == IT_STOP) break;
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Decisions.  Exact: row statistics from the A-item partials (fixed order,
+// fp64), tau at every drafted position from the gathered logits (fp64;
+// activation.cpp:20-27 + verify_reference.cpp:87-92), first rejection
+// (verify_reference.cpp:93-96, inclusive u <= tau).
+template <typename T>
+__device__ void decide_exact(const StepParams& P, int b, double* s_red, int* s_ired, double2* s_rs) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int G = P.G;
-    for (int r = warp; r < P.NR; r += kWarps) {
-        const double2* part = P.part + ((size_t)b * P.NR + r) * P.K;
-        double m = -CUDART_INF;
-        for (int k = lane; k < P.K; k += 32) m = fmax(m, __ldcg(&part[k].x));
-        m = warp_max(m);
-        double s = 0.0;
-        for (int k = lane; k < P.K; k += 32) {
-            const double2 pk = __ldcg(&part[k]);
-            if (pk.y > 0.0) s += pk.y * exp(pk.x - m);
-        }
-        s = warp_sum(s);
-        if (lane == 0) P.rowstat[(size_t)b * P.NR + r] = make_double2(m, s);
-    }
-    __syncthreads();
-    const double2* rs = P.rowstat + (size_t)b * P.NR;
-    for (int c = threadIdx.x; c < G; c += kThreads) {
+    // gathers and uniforms first: their latency overlaps the row statistics
+    const int c = threadIdx.x;
+    double zp = 0.0, zq = 0.0, u = 0.0;
+    if (c < G) {
         int x = P.ids[(size_t)b * G + c];
         if (x < 0 || x >= P.V) {
             flag(P, SSV_STATUS_TOKEN_RANGE);
             x = x < 0 ? 0 : P.V - 1;
         }
-        const double2 sp = rs[c], sq = rs[G + c];
-        const double zp = load_exact(p_row<T>(P, b, c) + x);
-        const double zq = load_exact(q_row<T>(P, b, c) + x);
-        const double p = exp(zp - sp.x) / sp.y;
-        const double q = exp(zq - sq.x) / sq.y;
-        P.tau[(size_t)b * G + c] = ratio_clamped(p, q);
+        zp = load_exact(p_row<T>(P, b, c) + x);
+        zq = load_exact(q_row<T>(P, b, c) + x);
     }
-    if (P.check_uniforms) {
-        for (int c = threadIdx.x; c <= G; c += kThreads) {
-            const double u = P.u[(size_t)b * (G + 1) + c];
-            if (!(u >= 0.0) || !(u < 1.0)) flag(P, SSV_STATUS_UNIFORM_RANGE);
+    if (c <= G) u = P.u[(size_t)b * (G + 1) + c];
+    if (P.check_uniforms && c <= G && (!(u >= 0.0) || !(u < 1.0))) flag(P, SSV_STATUS_UNIFORM_RANGE);
+    for (int r = warp; r < P.NR; r += kConsWarps) {
+        const double2* part = P.part + ((size_t)b * P.NR + r) * P.RPR;
+        double2 pk[4];
+        double m = -CUDART_INF;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int k = lane + 32 * i;
+            pk[i] = k < P.RPR ? __ldcg(&part[k]) : make_double2(-CUDART_INF, 0.0);
+            m = fmax(m, pk[i].x);
+        }
+        for (int k = lane + 128; k < P.RPR; k += 32) m = fmax(m, __ldcg(&part[k].x));
+        m = warp_max(m);
+        double sm = 0.0;
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+            if (pk[i].y > 0.0) sm += pk[i].y * exp(pk[i].x - m);
+        for (int k = lane + 128; k < P.RPR; k += 32) {
+            const double2 v = __ldcg(&part[k]);
+            if (v.y > 0.0) sm += v.y * exp(v.x - m);
+        }
+        sm = warp_sum(sm);
+        if (lane == 0) {
+            P.rowstat[(size_t)b * P.NR + r] = make_double2(m, sm);
+            if (r < kMaxRowsSmem) s_rs[r] = make_double2(m, sm);
         }
     }
-    __syncthreads();
+    cbar<kCons>();
+    auto rs = [&](int r) -> double2 { return r < kMaxRowsSmem ? s_rs[r] : P.rowstat[(size_t)b * P.NR + r]; };
+    int rej = 0x7fffffff;
+    if (c < G) {
+        const double2 sp = rs(c), sq = rs(G + c);
+        const double p = exp(zp - sp.x) / sp.y;   // activation.cpp:20-27, dist.cpp:46-50
+        const double q = exp(zq - sq.x) / sq.y;
+        const double tau = ratio_clamped(p, q);
+        P.tau[(size_t)b * G + c] = tau;
+        if (!(u <= tau)) rej = c;                // verify_reference.cpp:93-96 (inclusive)
+    }
+    const int a = min(creduce(rej, s_ired, OpMin()), G);
     if (threadIdx.x == 0) {
-        const double* u = P.u + (size_t)b * (G + 1);
-        const double* tau = P.tau + (size_t)b * G;
-        int a = 0;
-        while (a < G && u[a] <= tau[a]) ++a;
         P.acc[b] = a;
         Decision d{};
         if (a < G) {
+            const double2 sp = rs(a), sq = rs(G + a);
             d.mode = MODE_REJECT;
             d.row = a;
-            d.Mp = rs[a].x;
-            d.Sp = rs[a].y;
-            d.Mq = rs[G + a].x;
-            d.Sq = rs[G + a].y;
+            d.Mp = sp.x;
+            d.Sp = sp.y;
+            d.Mq = sq.x;
+            d.Sq = sq.y;
         } else if (P.PS == G + 1) {
             d.mode = MODE_BONUS;
             d.row = G;
@@ -214,74 +473,17 @@ __device__ void decide_softmax(const StepParams& P, int b) {
             P.rden[b] = 0.0;
         }
         P.dec[b] = d;
-    }
-}
-
-template <typename T, int NV>
-__global__ void __launch_bounds__(kThreads) k_row_stats(StepParams P) {
-    using A = typename Elem<T>::acc;
-    constexpr int W = 32 * NV * Elem<T>::VEC;  // elements per warp
-    const int warp = threadIdx.x >> 5;
-    const int task = blockIdx.x;
-    const int k = task % P.K;
-    const int br = task / P.K;
-    const int r = br % P.NR;
-    const int b = br / P.NR;
-    const T* row = stat_row<T>(P, b, r);
-    const int lo = min(k * P.CH + warp * W, P.V);
-    const int hi = min(lo + W, P.V);
-
-    WarpTile<T, NV> t;
-    t.load(row, lo, hi);
-    A mx = -CUDART_INF_F, mn = CUDART_INF_F;
-    if constexpr (sizeof(A) == 8) {
-        mx = -CUDART_INF;
-        mn = CUDART_INF;
-    }
-    t.minmax(mx, mn);
-
-    __shared__ A s_mx[kWarps], s_mn[kWarps];
-    __shared__ double s_sum[kWarps];
-    __shared__ bool s_last;
-    mx = warp_max(mx);
-    mn = warp_min(mn);
-    if ((threadIdx.x & 31) == 0) {
-        s_mx[warp] = mx;
-        s_mn[warp] = mn;
-    }
-    __syncthreads();
-    A M = s_mx[0], MN = s_mn[0];
-#pragma unroll
-    for (int w = 1; w < kWarps; ++w) {
-        M = fmax(M, s_mx[w]);
-        MN = fmin(MN, s_mn[w]);
-    }
-    double s = warp_sum(t.sum_exp(M));
-    if ((threadIdx.x & 31) == 0) s_sum[warp] = s;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        double S = 0.0;
-#pragma unroll
-        for (int w = 0; w < kWarps; ++w) S += s_sum[w];
-        P.part[task] = make_double2((double)M, S);
-        if (!isfinite((double)M) || isnan(S) || !isfinite((double)MN)) flag(P, SSV_STATUS_NONFINITE);
+        P.cnt1[b] = 0;  // every A-item of b has been counted (the producer waited for it)
         __threadfence();
-        const unsigned prev = atomicAdd(&P.cnt1[b], 1u);
-        s_last = (prev == (unsigned)(P.NR * P.K - 1));
+        st_release(&P.flag[b], P.epoch);
     }
-    __syncthreads();
-    if (!s_last) return;
-    __threadfence();
-    if (threadIdx.x == 0) P.cnt1[b] = 0;  // self-resetting for the next call
-    decide_softmax<T>(P, b);
 }
 
-// ---------------------------------------------------------------------------
-// Gathered-logit decision for the sigmoid / probability variants (one warp).
+// Sigmoid / probability decision from the gathered logits only (one warp).
 // verify_sigmoid.cpp:50-58 -> verify_reference.cpp:87-96; the sigmoid is
 // evaluated in fp64 exactly as dist.cpp:60-62 does.
 template <typename T, int ACT>
-__device__ void decide_gather(const StepParams& P, int b, bool write, int& mode, int& row) {
+__device__ void decide_gather(const StepParams& P, int b) {
     const int lane = threadIdx.x & 31;
     const int G = P.G;
     int accepted = G;
@@ -291,7 +493,7 @@ __device__ void decide_gather(const StepParams& P, int b, bool write, int& mode,
         if (c < G) {
             int x = P.ids[(size_t)b * G + c];
             if (x < 0 || x >= P.V) {
-                if (write) flag(P, SSV_STATUS_TOKEN_RANGE);
+                flag(P, SSV_STATUS_TOKEN_RANGE);
                 x = x < 0 ? 0 : P.V - 1;
             }
             const double zp = load_exact(p_row<T>(P, b, c) + x);
@@ -303,10 +505,10 @@ __device__ void decide_gather(const StepParams& P, int b, bool write, int& mode,
             } else {
                 p = zp;
                 q = zq;
-                if (write && (p < 0.0 || q < 0.0)) flag(P, SSV_STATUS_NEGATIVE);
+                if (p < 0.0 || q < 0.0) flag(P, SSV_STATUS_NEGATIVE);
             }
             const double tau = ratio_clamped(p, q);
-            if (write) P.tau[(size_t)b * G + c] = tau;
+            P.tau[(size_t)b * G + c] = tau;
             rej = !(P.u[(size_t)b * (G + 1) + c] <= tau);
         }
         const unsigned m = __ballot_sync(kFull, rej);
@@ -315,50 +517,46 @@ __device__ void decide_gather(const StepParams& P, int b, bool write, int& mode,
             break;
         }
     }
-    if (write && P.check_uniforms) {
+    if (P.check_uniforms) {
         for (int c = lane; c <= G; c += 32) {
             const double u = P.u[(size_t)b * (G + 1) + c];
             if (!(u >= 0.0) || !(u < 1.0)) flag(P, SSV_STATUS_UNIFORM_RANGE);
         }
     }
-    if (accepted < G) {
-        mode = MODE_REJECT;
-        row = accepted;
-    } else if (P.PS == G + 1) {
-        mode = MODE_BONUS;
-        row = G;
-    } else {
-        mode = MODE_NONE;
-        row = -1;
-    }
-    if (write && lane == 0) {
+    if (lane == 0) {
+        Decision d{};
+        d.Sp = d.Sq = 1.0;
         P.acc[b] = accepted;
-        if (mode == MODE_NONE) {
+        if (accepted < G) {
+            d.mode = MODE_REJECT;
+            d.row = accepted;
+        } else if (P.PS == G + 1) {
+            d.mode = MODE_BONUS;
+            d.row = G;
+        } else {
+            d.mode = MODE_NONE;
             P.fin[b] = -1;
             P.rsu[b] = 0;
             P.rden[b] = 0.0;
         }
+        P.dec[b] = d;
+        __threadfence();
+        st_release(&P.flag[b], P.epoch);
     }
 }
 
 // ---------------------------------------------------------------------------
 // Per-element values.  Streaming (acc precision) and exact (fp64) forms.
 struct RowCtx {
-    int mode;         // MODE_REJECT / MODE_BONUS
-    bool useA;        // reject: sample the residual (else the degenerate fallback on p)
+    int mode;   // MODE_REJECT / MODE_BONUS
+    bool useA;  // reject: sample the residual (else the degenerate fallback on p)
     double Mp, Sp, Mq, Sq;
     double denom;
 };
 
-template <typename T, int ACT>
-__device__ __forceinline__ double exact_p(const StepParams& P, const RowCtx& R, double z) {
-    if (ACT == ACT_SOFTMAX) return exp(z - R.Mp) / R.Sp;     // dist.cpp:46-50
-    if (ACT == ACT_SIGMOID) return sigmoid_scaled_d(z, P.alpha, P.width);
-    return z;
-}
-template <typename T, int ACT>
-__device__ __forceinline__ double exact_q(const StepParams& P, const RowCtx& R, double z) {
-    if (ACT == ACT_SOFTMAX) return exp(z - R.Mq) / R.Sq;
+template <int ACT>
+__device__ __forceinline__ double exact_act(const StepParams& P, double z, double M, double S) {
+    if (ACT == ACT_SOFTMAX) return exp(z - M) / S;  // dist.cpp:46-50
     if (ACT == ACT_SIGMOID) return sigmoid_scaled_d(z, P.alpha, P.width);
     return z;
 }
@@ -366,11 +564,11 @@ __device__ __forceinline__ double exact_q(const StepParams& P, const RowCtx& R, 
 // Value the inverse CDF scans at element i (fp64): residual max(0, p - q)
 // (verify_reference.cpp:51-55) or the p row itself (fallback / bonus).
 template <typename T, int ACT>
-__device__ __forceinline__ double exact_value(const StepParams& P, const RowCtx& R, const T* pr,
-                                              const T* qr, int i) {
-    const double p = exact_p<T, ACT>(P, R, load_exact(pr + i));
+__device__ __forceinline__ double exact_value(const StepParams& P, const RowCtx& R, const T* pr, const T* qr,
+                                              int i) {
+    const double p = exact_act<ACT>(P, load_exact(pr + i), R.Mp, R.Sp);
     if (R.mode == MODE_REJECT && R.useA) {
-        const double q = exact_q<T, ACT>(P, R, load_exact(qr + i));
+        const double q = exact_act<ACT>(P, load_exact(qr + i), R.Mq, R.Sq);
         const double d = p - q;
         return d > 0.0 ? d : 0.0;
     }
@@ -378,36 +576,39 @@ __device__ __forceinline__ double exact_value(const StepParams& P, const RowCtx&
 }
 
 // ---------------------------------------------------------------------------
-// K2 epilogue: inverse CDF of batch row b over the granule partials, then an
-// exact fp64 scan inside the selected granule (dist.cpp:122-137).
+// Inverse CDF of batch row b (consumer group): granule partials -> SMEM ->
+// fp64 granule prefix (contiguous ownership, one scan) -> exact fp64 scan
+// inside the selected granule (dist.cpp:122-137, incl. both fallbacks).
 template <typename T, int ACT>
-__device__ void locate(const StepParams& P, int b, int mode, int row, const double* st) {
-    __shared__ double s_red[kWarps];
-    __shared__ int s_ired[kWarps];
-    const int NG = P.NG;
+__device__ void locate(const StepParams& P, const Slot& it, double2* gcache, double* s_red, int* s_ired) {
+    const int b = it.b, NG = P.NG, GW = P.GW;
     const double2* gp = P.gpart + (size_t)b * NG;
-    const T* pr = p_row<T>(P, b, row);
-    const T* qr = (mode == MODE_REJECT) ? q_row<T>(P, b, row) : nullptr;
-    const double u = P.u[(size_t)b * (P.G + 1) + P.G];  // u_final, verify_reference.cpp:98
+    const T* pr = p_row<T>(P, b, it.row);
+    const T* qr = it.mode == MODE_REJECT ? q_row<T>(P, b, it.row) : nullptr;
+    const double u = __ldcg(&P.u[(size_t)b * (P.G + 1) + P.G]);  // u_final, verify_reference.cpp:98
+    const int ncache = min(NG, kLocCap);
+    for (int g = threadIdx.x; g < ncache; g += kCons) gcache[g] = __ldcg(&gp[g]);
+    cbar<kCons>();
+    auto raw = [&](int g) -> double2 { return g < kLocCap ? gcache[g] : __ldcg(&gp[g]); };
 
     RowCtx R;
-    R.mode = mode;
-    R.Mp = st[0];
-    R.Sp = st[1];
-    R.Mq = st[2];
-    R.Sq = st[3];
+    R.mode = it.mode;
+    R.Mp = it.Mp;
+    R.Sp = it.Sp;
+    R.Mq = it.Mq;
+    R.Sq = it.Sq;
     R.useA = false;
-    double gM = 0.0, gS = 1.0;  // softmax bonus: row max / sum from the granule partials
-
-    if (mode == MODE_REJECT) {
+    R.denom = 1.0;
+    double gM = 0.0, gS = 1.0;
+    if (it.mode == MODE_REJECT) {
         double sa = 0.0, sp = 0.0;
-        for (int g = threadIdx.x; g < NG; g += kThreads) {
-            const double2 v = __ldcg(&gp[g]);
+        for (int g = threadIdx.x; g < NG; g += kCons) {
+            const double2 v = raw(g);
             sa += v.x;
             sp += v.y;
         }
-        sa = block_reduce(sa, s_red, OpSum());
-        sp = block_reduce(sp, s_red, OpSum());
+        sa = creduce(sa, s_red, OpSum());
+        sp = creduce(sp, s_red, OpSum());
         R.useA = sa > kZeroEps;  // verify_reference.cpp:57-62
         R.denom = R.useA ? sa : sp;
         if (threadIdx.x == 0) {
@@ -415,289 +616,412 @@ __device__ void locate(const StepParams& P, int b, int mode, int row, const doub
             if (P.rden) P.rden[b] = R.useA ? sa : 0.0;
         }
     } else {
-        if (ACT == ACT_SOFTMAX) {
+        if (ACT == ACT_SOFTMAX) {  // the bonus row's statistics from its granules
             double m = -CUDART_INF;
-            for (int g = threadIdx.x; g < NG; g += kThreads) m = fmax(m, __ldcg(&gp[g].x));
-            gM = block_reduce(m, s_red, OpMax());
-            double s = 0.0;
-            for (int g = threadIdx.x; g < NG; g += kThreads) {
-                const double2 v = __ldcg(&gp[g]);
-                if (v.y > 0.0) s += v.y * exp(v.x - gM);
+            for (int g = threadIdx.x; g < NG; g += kCons) m = fmax(m, raw(g).x);
+            gM = creduce(m, s_red, OpMax());
+            double sm = 0.0;
+            for (int g = threadIdx.x; g < NG; g += kCons) {
+                const double2 v = raw(g);
+                if (v.y > 0.0) sm += v.y * exp(v.x - gM);
             }
-            gS = block_reduce(s, s_red, OpSum());
+            gS = creduce(sm, s_red, OpSum());
             R.Mp = gM;
             R.Sp = gS;
+            R.denom = 1.0;  // sample_row's sequential_sum of a softmax row (1 within rounding)
+        } else {
+            double sm = 0.0;
+            for (int g = threadIdx.x; g < NG; g += kCons) sm += raw(g).y;
+            R.denom = creduce(sm, s_red, OpSum());
         }
         if (threadIdx.x == 0) {
             if (P.rsu) P.rsu[b] = 0;
             if (P.rden) P.rden[b] = 0.0;
         }
     }
-    // Granule mass in the units the scan uses.
-    auto gmass = [&](int g) -> double {
-        const double2 v = __ldcg(&gp[g]);
-        if (mode == MODE_REJECT) return R.useA ? v.x : v.y;
+    auto gmass = [&](int g) -> double {  // normalized granule mass
+        const double2 v = raw(g);
+        if (R.mode == MODE_REJECT) return (R.useA ? v.x : v.y) / R.denom;
         if (ACT == ACT_SOFTMAX) return v.y > 0.0 ? v.y * exp(v.x - gM) / gS : 0.0;
-        return v.y;
+        return v.y / R.denom;
     };
-    if (mode == MODE_BONUS) {
-        double s = 0.0;
-        for (int g = threadIdx.x; g < NG; g += kThreads) s += gmass(g);
-        R.denom = block_reduce(s, s_red, OpSum());  // sample_row's sequential_sum, ~1 for softmax
-    }
 
-    // Level 1: first granule whose normalized prefix exceeds u.
-    double carry = 0.0;
-    int gstar = -1;
-    for (int g0 = 0; g0 < NG && gstar < 0; g0 += kThreads) {
-        const int g = g0 + threadIdx.x;
-        const double w = g < NG ? gmass(g) / R.denom : 0.0;
-        double total;
-        const double incl = carry + block_scan_incl(w, s_red, total);
-        const int hit = (g < NG && u < incl) ? g : 0x7fffffff;
-        const int first = block_reduce(hit, s_ired, OpMin());
-        if (first != 0x7fffffff) {
-            gstar = first;
-            // carry before gstar = incl(gstar) - w(gstar); recompute exactly
-            if (threadIdx.x == first - g0) s_red[0] = incl - w;
-            __syncthreads();
-            carry = s_red[0];
-            __syncthreads();
-        } else {
-            carry += total;
+    // Level 1: contiguous granule ownership, one block scan.
+    const int gpt = (NG + kCons - 1) / kCons;
+    const int ga = min(NG, threadIdx.x * gpt), gb = min(NG, ga + gpt);
+    double tsum = 0.0;
+    for (int g = ga; g < gb; ++g) tsum += gmass(g);
+    double total;
+    double run = cscan_incl(tsum, s_red, total) - tsum;
+    int hit = 0x7fffffff;
+    double hit_carry = 0.0;
+    for (int g = ga; g < gb; ++g) {
+        const double w = gmass(g);
+        if (u < run + w) {
+            hit = g;
+            hit_carry = run;
+            break;
         }
+        run += w;
+    }
+    int gstar = creduce(hit, s_ired, OpMin());
+    double carry = 0.0;
+    if (gstar != 0x7fffffff) {
+        if (hit == gstar) s_red[0] = hit_carry;  // creduce's barriers ordered every earlier s_red read
+        cbar<kCons>();
+        carry = s_red[0];
+    } else {
+        gstar = -1;
     }
 
     // Level 2: exact element scan, continuing into later granules on rounding.
-    constexpr int E2 = kGranule / kThreads;
     int token = -1;
+    const int E = (GW + kCons - 1) / kCons;  // elements per thread (1 or 2)
     while (gstar >= 0 && gstar < NG) {
-        const int lo = gstar * kGranule;
-        const int base = lo + threadIdx.x * E2;
-        double vals[E2];
-        double tsum = 0.0;
-#pragma unroll
-        for (int e = 0; e < E2; ++e) {
-            const int i = base + e;
-            vals[e] = (i < P.V) ? exact_value<T, ACT>(P, R, pr, qr, i) / R.denom : 0.0;
-            tsum += vals[e];
-        }
-        double total;
-        const double incl = block_scan_incl(tsum, s_red, total);
-        double cum = carry + (incl - tsum);
-        int hit = 0x7fffffff;
-#pragma unroll
-        for (int e = 0; e < E2; ++e) {
-            cum += vals[e];
-            if (hit == 0x7fffffff && base + e < P.V && u < cum) hit = base + e;
-        }
-        const int first = block_reduce(hit, s_ired, OpMin());
+        const int lo = gstar * GW;
+        const int hi = min(lo + GW, P.V);
+        const int base = lo + threadIdx.x * E;
+        double v0 = 0.0, v1 = 0.0;
+        if (base < hi) v0 = exact_value<T, ACT>(P, R, pr, qr, base) / R.denom;
+        if (E > 1 && base + 1 < hi) v1 = exact_value<T, ACT>(P, R, pr, qr, base + 1) / R.denom;
+        const double ts = v0 + v1;
+        double tot;
+        const double incl = cscan_incl(ts, s_red, tot);
+        double cum = carry + (incl - ts);
+        int h = 0x7fffffff;
+        cum += v0;
+        if (base < hi && u < cum) h = base;
+        cum += v1;
+        if (h == 0x7fffffff && E > 1 && base + 1 < hi && u < cum) h = base + 1;
+        const int first = creduce(h, s_ired, OpMin());
         if (first != 0x7fffffff) {
             token = first;
             break;
         }
-        carry += total;
+        carry += tot;
         ++gstar;
     }
     if (token < 0) {
         // dist.cpp:135-136: last index with positive mass, else 0.
         int glast = -1;
-        for (int g = threadIdx.x; g < NG; g += kThreads)
+        for (int g = threadIdx.x; g < NG; g += kCons)
             if (gmass(g) > 0.0) glast = max(glast, g);
-        glast = block_reduce(glast, s_ired, OpMax());
+        glast = creduce(glast, s_ired, OpMax());
         token = 0;
         if (glast >= 0) {
             int last = -1;
-            for (int i = glast * kGranule + threadIdx.x; i < min((glast + 1) * kGranule, P.V); i += kThreads)
+            for (int i = glast * GW + threadIdx.x; i < min((glast + 1) * GW, P.V); i += kCons)
                 if (exact_value<T, ACT>(P, R, pr, qr, i) > 0.0) last = max(last, i);
-            last = block_reduce(last, s_ired, OpMax());
+            last = creduce(last, s_ired, OpMax());
             if (last >= 0) token = last;
         }
     }
-    if (threadIdx.x == 0) P.fin[b] = token;
+    if (threadIdx.x == 0) {
+        P.fin[b] = token;
+        P.cnt2[b] = 0;  // every B-item of b has been counted (the producer waited for it)
+    }
 }
 
 // ---------------------------------------------------------------------------
-// Granule partials of one warp.
-template <typename T, int ACT>
-__device__ __forceinline__ double2 granule_partial(const StepParams& P, const RowCtx& R,
-                                                   const T* pr, const T* qr, int lo, int hi) {
-    using A = typename Elem<T>::acc;
-    constexpr int VEC = Elem<T>::VEC;
-    constexpr int NV = kGranule / (32 * VEC);
-    const int lane = threadIdx.x & 31;
-    const A alpha = (A)P.alpha, invw = (A)(1.0 / P.width);
-
-    // streaming value of p (acc precision)
-    auto vp_of = [&](A x) -> A {
-        if (ACT == ACT_SOFTMAX) return exp_rel(x, (A)R.Mp) * (A)(1.0 / R.Sp);
-        if (ACT == ACT_SIGMOID) return (A)1 / ((A)1 + exp_neg((x - alpha) * invw));
-        return x;
-    };
-
-    if (R.mode == MODE_BONUS) {
-        WarpTile<T, NV> t;
-        t.load(pr, lo, hi);
-        if (ACT == ACT_SOFTMAX) {
-            A mx = -INFINITY, mn = INFINITY;
-            t.minmax(mx, mn);
-            mx = warp_max(mx);
-            const double s = warp_sum(t.sum_exp(mx));
-            return make_double2((double)mx, s);
-        }
-        const double s = warp_sum(t.sum_map(vp_of));
-        return make_double2(0.0, s);
-    }
-
-    // Residual pair: a = max(0, p - q) and the fallback mass sum p.
-    auto pair = [&](A xp, A xq, A& a, A& vp) {
-        if (ACT == ACT_SOFTMAX) {
-            vp = exp_rel(xp, (A)R.Mp) * (A)(1.0 / R.Sp);
-            const A vq = exp_rel(xq, (A)R.Mq) * (A)(1.0 / R.Sq);
-            a = vp - vq > (A)0 ? vp - vq : (A)0;
-        } else if (ACT == ACT_SIGMOID) {
-            // sigma(tp) - sigma(tq) = sigma(tp) * sigma(-tq) * (1 - e^-(tp-tq)), no cancellation.
-            const A tp = (xp - alpha) * invw, tq = (xq - alpha) * invw;
-            const A d = (xp - xq) * invw;
-            vp = (A)1 / ((A)1 + exp_neg(tp));
-            const A sq_neg = (A)1 / ((A)1 + exp_neg(-tq));
-            a = d > (A)0 ? vp * sq_neg * (-expm1_acc(-d)) : (A)0;
-        } else {
-            vp = xp;
-            a = xp - xq > (A)0 ? xp - xq : (A)0;
-        }
-    };
-
-    double sa = 0.0, sp = 0.0;
-    const bool vec_ok = ((reinterpret_cast<uintptr_t>(pr) | reinterpret_cast<uintptr_t>(qr)) & 15) == 0 &&
-                        (P.V % VEC) == 0;
-    if (vec_ok) {
-        const int nvec = (hi - lo) / VEC;  // lo and V are multiples of VEC
-        uint4 vp4[NV], vq4[NV];
-#pragma unroll
-        for (int j = 0; j < NV; ++j) {
-            const int idx = j * 32 + lane;
-            if (idx < nvec) {
-                vp4[j] = ldg_stream(pr + lo + (size_t)idx * VEC);
-                vq4[j] = ldg_stream(qr + lo + (size_t)idx * VEC);
-            }
-        }
-#pragma unroll
-        for (int j = 0; j < NV; ++j) {
-            if (j * 32 + lane < nvec) {
-                A xp[VEC], xq[VEC];
-                unpack(vp4[j], xp);
-                unpack(vq4[j], xq);
-                A ta = 0, tp = 0;
-#pragma unroll
-                for (int e = 0; e < VEC; ++e) {
-                    A a, v;
-                    pair(xp[e], xq[e], a, v);
-                    ta += a;
-                    tp += v;
-                }
-                sa += (double)ta;
-                sp += (double)tp;
-            }
-        }
-    } else {
-        constexpr int NS = kGranule / 32;
-        A xp[NS], xq[NS];
-#pragma unroll
-        for (int j = 0; j < NS; ++j) {
-            const int i = lo + j * 32 + lane;
-            if (i < hi) {
-                xp[j] = load_elem(pr + i);
-                xq[j] = load_elem(qr + i);
-            }
-        }
-        A ta = 0, tp = 0;
-#pragma unroll
-        for (int j = 0; j < NS; ++j) {
-            if (lo + j * 32 + lane < hi) {
-                A a, v;
-                pair(xp[j], xq[j], a, v);
-                ta += a;
-                tp += v;
-            }
-            if ((j & 7) == 7) {
-                sa += (double)ta;
-                sp += (double)tp;
-                ta = 0;
-                tp = 0;
-            }
-        }
-        sa += (double)ta;
-        sp += (double)tp;
-    }
-    return make_double2(warp_sum(sa), warp_sum(sp));
+__device__ __forceinline__ void red_release_add(unsigned* p, unsigned v) {
+    asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
-template <typename T, int ACT>
-__global__ void __launch_bounds__(kThreads) k_row_pass(StepParams P) {
-    const int b = blockIdx.y;
-    const int warp = threadIdx.x >> 5;
-    __shared__ int s_mode, s_row;
-    __shared__ double s_st[4];
-    __shared__ bool s_last;
+// Lane 0 of each warp counts the warp out of run `ri`; true in exactly one
+// warp per run (the last), after every other warp's writes to `ri`.
+__device__ __forceinline__ bool run_last_warp(RunInfo& ri) {
+    unsigned old = 0;
+    if ((threadIdx.x & 31) == 0) {
+        __threadfence_block();
+        old = atomicAdd(&ri.cnt, 1u);
+        __threadfence_block();
+    }
+    old = __shfl_sync(kFull, old, 0);
+    return old == kConsWarps - 1;
+}
 
-    if (P.sample_mode) {
-        if (threadIdx.x == 0) {
-            s_mode = MODE_BONUS;
-            s_row = 0;
+// Per-lane online softmax state of the A-run in flight.
+template <typename A>
+struct LaneRun {
+    A m, mn;
+    double s;
+};
+
+// A-chunk: the warp copies its 1/8 of the staged chunk into registers, frees
+// the stage, then folds it into the lane's running (max, sum e^(x - max), min)
+// -- fp32 ex2 within the chunk, fp64 across chunks, an fp64 exp only when the
+// lane's max grows.  No cross-lane work until the run's last chunk.
+template <typename T>
+__device__ __forceinline__ void chunk_A(const StepParams& P, const uint8_t* st, int shift, int n,
+                                        LaneRun<typename Elem<T>::acc>& L, uint64_t* empty_s) {
+    using A = typename Elem<T>::acc;
+    constexpr int VEC = Elem<T>::VEC;
+    constexpr int WPW = kStageBytes / 16 / kConsWarps;  // 16-byte words per warp (128)
+    constexpr int M = WPW / 32;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int end = shift + n;                          // valid element range in the stage
+    const int nwords = (end * (int)sizeof(T) + 15) / 16;  // <= 1025
+    const int w0 = warp * WPW;
+    const int w1 = min(nwords, w0 + WPW);
+    uint4 w[M];
+    uint4 wx;  // the 1025th word of a misaligned chunk (warp 7, lane 0)
+    const bool has_x = warp == kConsWarps - 1 && lane == 0 && nwords > kConsWarps * WPW;
+#pragma unroll
+    for (int m = 0; m < M; ++m) {
+        const int wi = w0 + lane + 32 * m;
+        if (wi < w1) w[m] = *reinterpret_cast<const uint4*>(st + (size_t)wi * 16);
+    }
+    if (has_x) wx = *reinterpret_cast<const uint4*>(st + (size_t)(kConsWarps * WPW) * 16);
+    __syncwarp();
+    if (lane == 0) mbar_arrive(empty_s);  // the stage is free for the producer
+    A cm = -INFINITY, cn = INFINITY;
+    auto scan_word = [&](const uint4& v, int wi, auto&& f) {
+        A x[VEC];
+        unpack(v, x);
+        if (wi * VEC >= shift && (wi + 1) * VEC <= end) {
+#pragma unroll
+            for (int e = 0; e < VEC; ++e) f(x[e]);
+        } else {
+#pragma unroll
+            for (int e = 0; e < VEC; ++e) {
+                const int idx = wi * VEC + e;
+                if (idx >= shift && idx < end) f(x[e]);
+            }
         }
-    } else if (ACT == ACT_SOFTMAX) {
-        if (threadIdx.x == 0) {
-            const Decision d = P.dec[b];
-            s_mode = d.mode;
-            s_row = d.row;
-            s_st[0] = d.Mp;
-            s_st[1] = d.Sp;
-            s_st[2] = d.Mq;
-            s_st[3] = d.Sq;
+    };
+    auto mm = [&](A x) {
+        cm = fmax(cm, x);
+        cn = fmin(cn, x);
+    };
+#pragma unroll
+    for (int m = 0; m < M; ++m) {
+        const int wi = w0 + lane + 32 * m;
+        if (wi < w1) scan_word(w[m], wi, mm);
+    }
+    if (has_x) scan_word(wx, kConsWarps * WPW, mm);
+    if (cm > L.m) {  // the lane's max grew: rescale its running sum (fp64)
+        if (L.s > 0.0) L.s *= exp((double)L.m - (double)cm);
+        L.m = cm;
+    }
+    L.mn = fmin(L.mn, cn);
+    if (L.m > -INFINITY) {
+        A t = 0;
+        const A mref = L.m;
+        auto ex = [&](A x) { t += exp_rel(x, mref); };
+#pragma unroll
+        for (int m = 0; m < M; ++m) {
+            const int wi = w0 + lane + 32 * m;
+            if (wi < w1) scan_word(w[m], wi, ex);
         }
-    } else if (warp == 0) {
-        int mode, row;
-        decide_gather<T, ACT>(P, b, blockIdx.x == 0, mode, row);
-        if (threadIdx.x == 0) {
-            s_mode = mode;
-            s_row = row;
-            s_st[0] = s_st[2] = 0.0;
-            s_st[1] = s_st[3] = 1.0;
+        if (has_x) scan_word(wx, kConsWarps * WPW, ex);
+        L.s += (double)t;
+    }
+}
+
+// End of an A-run: warp partial, and the run's last warp folds the 8 warp
+// partials (fixed order) and publishes ONE (max, sum) per run.
+template <typename A>
+__device__ void finish_A(const StepParams& P, RunInfo& ri, LaneRun<A>& L) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (isnan(L.s)) flag(P, SSV_STATUS_NONFINITE);  // NaN logit (require_finite, dist.cpp:27-36)
+    const double lm = (double)L.m;
+    const double M = warp_max(lm);
+    const double S = warp_sum(L.s > 0.0 ? L.s * exp(lm - M) : 0.0);
+    const double MN = warp_min((double)L.mn);
+    if (lane == 0) {
+        if (isnan(S)) flag(P, SSV_STATUS_NONFINITE);  // NaN logit (require_finite, dist.cpp:27-36)
+        ri.wpart[warp] = make_double2(M, S);
+        ri.wmin[warp] = MN;
+    }
+    if (!run_last_warp(ri)) return;
+    const double2 wp = lane < kConsWarps ? ri.wpart[lane] : make_double2(-CUDART_INF, 0.0);
+    const double MX = warp_max(wp.x);
+    const double SX = warp_sum(wp.y > 0.0 ? wp.y * exp(wp.x - MX) : 0.0);
+    const double MNX = warp_min(lane < kConsWarps ? ri.wmin[lane] : CUDART_INF);
+    if (lane == 0) {
+        ri.cnt = 0;
+        P.part[((size_t)ri.b * P.NR + ri.r) * P.RPR + ri.q] = make_double2(MX, SX);
+        if (!isfinite(MX) || isnan(SX) || !isfinite(MNX)) flag(P, SSV_STATUS_NONFINITE);
+        __threadfence();
+        red_release_add(&P.cnt1[ri.b], 1u);
+    }
+}
+
+// B-chunk: each warp copies its granule (both rows for a rejection) into
+// registers, frees the stage, and reduces the granule; the run's last warp
+// publishes the run's granule partials.
+template <typename T, int ACT>
+__device__ void chunk_B(const StepParams& P, RunInfo& ri, const uint8_t* st, int pos, int n, uint64_t* empty_s) {
+    using A = typename Elem<T>::acc;
+    constexpr int EPL = kStageBytes / 2 / (int)sizeof(T) / kCons;  // elements per lane per granule
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int e0 = warp * P.GW;
+    const bool reject = ri.mode == MODE_REJECT;
+    const A alpha = (A)P.alpha, invw = (A)(1.0 / P.width);
+    A xs[EPL], xq[EPL];
+#pragma unroll
+    for (int t = 0; t < EPL; ++t) {
+        const int e = e0 + t * 32 + lane;
+        xs[t] = e < n ? lds_elem<T>(st, ri.shift_p + e) : (A)0;
+        xq[t] = (reject && e < n) ? lds_elem<T>(st + kHalfStride, ri.shift_q + e) : (A)0;
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(empty_s);
+    double2 out = make_double2(0.0, 0.0);
+    if (e0 < n) {
+        if (!reject) {
+            if (ACT == ACT_SOFTMAX) {
+                A mx = -INFINITY, mn = INFINITY;
+#pragma unroll
+                for (int t = 0; t < EPL; ++t)
+                    if (e0 + t * 32 + lane < n) {
+                        mx = fmax(mx, xs[t]);
+                        mn = fmin(mn, xs[t]);
+                    }
+                mx = warp_max(mx);
+                mn = warp_min(mn);
+                A sm = 0;
+#pragma unroll
+                for (int t = 0; t < EPL; ++t)
+                    if (e0 + t * 32 + lane < n) sm += exp_rel(xs[t], mx);
+                const double S = warp_sum((double)sm);
+                if (lane == 0 && (!isfinite((double)mx) || isnan(S) || !isfinite((double)mn)))
+                    flag(P, SSV_STATUS_NONFINITE);
+                out = make_double2((double)mx, S);
+            } else {
+                A sm = 0;
+#pragma unroll
+                for (int t = 0; t < EPL; ++t) {
+                    if (e0 + t * 32 + lane < n) {
+                        if (ACT == ACT_SIGMOID) sm += (A)1 / ((A)1 + exp_neg((xs[t] - alpha) * invw));
+                        else sm += xs[t];
+                    }
+                }
+                out = make_double2(0.0, warp_sum((double)sm));
+            }
+        } else {
+            const A Mp = (A)ri.Mp, Mq = (A)ri.Mq, iSp = (A)(1.0 / ri.Sp), iSq = (A)(1.0 / ri.Sq);
+            A ta = 0, tp = 0;
+#pragma unroll
+            for (int t = 0; t < EPL; ++t) {
+                if (e0 + t * 32 + lane < n) {
+                    const A xp = xs[t], xqq = xq[t];
+                    A a, vp;
+                    if (ACT == ACT_SOFTMAX) {
+                        vp = exp_rel(xp, Mp) * iSp;
+                        const A vq = exp_rel(xqq, Mq) * iSq;
+                        a = vp - vq > (A)0 ? vp - vq : (A)0;
+                    } else if (ACT == ACT_SIGMOID) {
+                        // sigma(tp) - sigma(tq) = sigma(tp) sigma(-tq) (1 - e^-(tp-tq)): no cancellation.
+                        const A tp_ = (xp - alpha) * invw, tq_ = (xqq - alpha) * invw;
+                        const A d = (xp - xqq) * invw;
+                        vp = (A)1 / ((A)1 + exp_neg(tp_));
+                        const A sqn = (A)1 / ((A)1 + exp_neg(-tq_));
+                        a = d > (A)0 ? vp * sqn * (-expm1_acc(-d)) : (A)0;
+                    } else {
+                        vp = xp;
+                        a = xp - xqq > (A)0 ? xp - xqq : (A)0;
+                    }
+                    ta += a;
+                    tp += vp;
+                }
+            }
+            out = make_double2(warp_sum((double)ta), warp_sum((double)tp));
         }
+    }
+    if (lane == 0) ri.gpart[pos * kConsWarps + warp] = out;
+    if (pos != ri.len - 1) return;
+    if (!run_last_warp(ri)) return;
+    const int g0 = ri.q * P.runB * kConsWarps;
+    const int ng = min(ri.len * kConsWarps, P.NG - g0);
+    for (int i = lane; i < ng; i += 32) P.gpart[(size_t)ri.b * P.NG + g0 + i] = ri.gpart[i];
+    __threadfence();
+    __syncwarp();
+    if (lane == 0) {
+        ri.cnt = 0;
+        red_release_add(&P.cnt2[ri.b], 1u);
+    }
+}
+
+// ---------------------------------------------------------------------------
+template <typename T, int ACT>
+__global__ void __launch_bounds__(kBlock, 2) k_verify(StepParams P) {
+    using A = typename Elem<T>::acc;
+    constexpr int CA = kStageBytes / (int)sizeof(T);
+    extern __shared__ __align__(128) uint8_t smem[];
+    uint8_t* stages = smem;
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)kStages * kStageStride);
+    uint64_t* empty = full + kStages;
+    Slot* slots = reinterpret_cast<Slot*>(empty + kStages);
+    double2* gcache = reinterpret_cast<double2*>(slots + kStages);
+    RunInfo* runs = reinterpret_cast<RunInfo*>(gcache + kLocCap);
+    __shared__ double s_red[kConsWarps];
+    __shared__ int s_ired[kConsWarps];
+    __shared__ double2 s_rs[kMaxRowsSmem];
+
+    if (threadIdx.x == 0) {
+        trace(P, 2 * blockIdx.x);
+        for (int s = 0; s < kStages; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], kConsWarps);  // every consumer warp frees the stage
+        }
+        for (int c = 0; c < kCtx; ++c) runs[c].cnt = 0;
+        mbar_fence_init();
     }
     __syncthreads();
-    const int mode = s_mode, row = s_row;
-    if (mode == MODE_NONE) return;
 
-    RowCtx R;
-    R.mode = mode;
-    R.Mp = s_st[0];
-    R.Sp = s_st[1];
-    R.Mq = s_st[2];
-    R.Sq = s_st[3];
-    const T* pr = p_row<T>(P, b, row);
-    const T* qr = mode == MODE_REJECT ? q_row<T>(P, b, row) : nullptr;
-
-    const int g = blockIdx.x * kWarps + warp;
-    if (g < P.NG) {
-        const int lo = g * kGranule;
-        const int hi = min(lo + kGranule, P.V);
-        const double2 part = granule_partial<T, ACT>(P, R, pr, qr, lo, hi);
-        if ((threadIdx.x & 31) == 0) P.gpart[(size_t)b * P.NG + g] = part;
+    if (threadIdx.x >= kCons) {
+        if (threadIdx.x == kCons) producer<T, ACT>(P, stages, full, empty, slots, runs);
+    } else {
+        const int lane = threadIdx.x & 31;
+        LaneRun<A> L{(A)-INFINITY, (A)INFINITY, 0.0};
+        unsigned n = 0;
+        for (;;) {
+            const unsigned s = n % kStages, ph = (n / kStages) & 1u;
+            mbar_wait(&full[s], ph);
+            const int4 hdr = *reinterpret_cast<const int4*>(&slots[s]);  // type, ctx, pos, b
+            ++n;
+            if (hdr.x == IT_STOP) break;
+            const uint8_t* st = stages + (size_t)s * kStageStride;
+            if (hdr.x == IT_A) {
+                RunInfo& ri = runs[hdr.y];
+                const int pos = hdr.z, len = ri.len;
+                const int lo = (ri.k0 + pos) * CA;
+                if (pos == 0) L = LaneRun<A>{(A)-INFINITY, (A)INFINITY, 0.0};
+                chunk_A<T>(P, st, ri.shift_p, min(CA, P.V - lo), L, &empty[s]);
+                if (pos == len - 1) finish_A<A>(P, ri, L);
+            } else if (hdr.x == IT_B) {
+                RunInfo& ri = runs[hdr.y];
+                const int lo = (ri.k0 + hdr.z) * P.CB;
+                chunk_B<T, ACT>(P, ri, st, hdr.z, min(P.CB, P.V - lo), &empty[s]);
+            } else {
+                const Slot sl = slots[s];
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&empty[s]);
+                cbar<kCons>();  // the decide / locate run on the whole consumer group
+                const int tb = 2 * (int)gridDim.x + 4 * sl.b + (sl.type == IT_D ? 0 : 2);
+                if (threadIdx.x == 0) trace(P, tb);
+                if (sl.type == IT_D) {
+                    if (ACT == ACT_SOFTMAX && !P.sample_mode) decide_exact<T>(P, sl.b, s_red, s_ired, s_rs);
+                    else if (threadIdx.x < 32) decide_gather<T, ACT>(P, sl.b);
+                } else {
+                    locate<T, ACT>(P, sl, gcache, s_red, s_ired);
+                }
+                if (threadIdx.x == 0) trace(P, tb + 1);
+            }
+        }
     }
-    __threadfence();
     __syncthreads();
     if (threadIdx.x == 0) {
-        const unsigned prev = atomicAdd(&P.cnt2[b], 1u);
-        s_last = (prev == gridDim.x - 1);
+        trace(P, 2 * blockIdx.x + 1);
+        __threadfence();
+        const unsigned prev = atomicAdd(P.exit_cnt, 1u);
+        if (prev == gridDim.x - 1) {  // last CTA out resets the work counters
+            *P.exit_cnt = 0;
+            *P.next = 0;
+            __threadfence();
+        }
     }
-    __syncthreads();
-    if (!s_last) return;
-    __threadfence();
-    if (threadIdx.x == 0) P.cnt2[b] = 0;
-    double st[4] = {s_st[0], s_st[1], s_st[2], s_st[3]};
-    locate<T, ACT>(P, b, mode, row, st);
 }
 
 // ---------------------------------------------------------------------------
@@ -808,53 +1132,96 @@ __global__ void k_gen_uniforms(uint64_t seed, int B, int G, int V, double* draft
 
 // ---------------------------------------------------------------------------
 // Host-side launchers.
-template <typename T, int NV>
-static void launch_stats_nv(const StepParams& P, const Launch& L) {
-    const long tasks = (long)P.B * P.NR * P.K;
-    const int h = L.begin(KID_ROW_STATS);
-    k_row_stats<T, NV><<<(unsigned)tasks, kThreads, 0, L.st>>>(P);
-    L.end(h);
-}
-
-template <typename T>
-static int stats_nv_for(const StepParams& P, int& CH) {
-    constexpr int VEC = Elem<T>::VEC;
-    const int nvs[3] = {8, 4, 2};
-    for (int i = 0; i < 3; ++i) {
-        const int ch = kWarps * 32 * nvs[i] * VEC;
-        const long tasks = (long)P.B * P.NR * ((P.V + ch - 1) / ch);
-        if (tasks >= 148L * 8 || i == 2) {
-            CH = ch;
-            return nvs[i];
-        }
+static int sm_count() {
+    static int n = 0;
+    if (n == 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        if (n <= 0) n = 148;
     }
-    return 2;
+    return n;
 }
 
-template <typename T>
-static void launch_stats_t(StepParams P, const Launch& L) {
-    int CH;
-    const int nv = stats_nv_for<T>(P, CH);
-    P.CH = CH;
-    P.K = (P.V + CH - 1) / CH;
-    if (nv == 8) launch_stats_nv<T, 8>(P, L);
-    else if (nv == 4) launch_stats_nv<T, 4>(P, L);
-    else launch_stats_nv<T, 2>(P, L);
+constexpr size_t kVerifySmem = (size_t)kStages * kStageStride + 2 * kStages * sizeof(uint64_t) +
+                               kStages * sizeof(Slot) + kLocCap * sizeof(double2) + kCtx * sizeof(RunInfo);
+
+static size_t elem_size(int dtype) { return dtype == DT_F64 ? 8 : (dtype == DT_BF16 ? 2 : 4); }
+
+void plan_geometry(int dtype, int act, StepParams& P) {
+    const int s = (int)elem_size(dtype);
+    const int CA = kStageBytes / s;
+    P.CH = CA;
+    P.CB = kStageBytes / (2 * s);
+    P.GW = P.CB / kConsWarps;
+    P.NG = (P.V + P.GW - 1) / P.GW;
+    P.nBi = (P.V + P.CB - 1) / P.CB;
+    if (P.sample_mode || act != ACT_SOFTMAX) {
+        P.NR = 0;
+        P.K = 0;
+    } else {
+        P.K = (P.V + CA - 1) / CA;
+    }
+    const long grid = 2L * sm_count();
+    // Runs: long enough to amortize one publish over many 16 KB chunks, short
+    // enough that every phase still spreads over ~4 runs per CTA.
+    auto run_len = [&](long chunks_per_row, long rows, int cap) {
+        if (chunks_per_row <= 0) return 1;
+        long want = (chunks_per_row * rows + 4 * grid - 1) / (4 * grid);
+        want = std::max<long>(1, std::min<long>({want, chunks_per_row, (long)cap}));
+        const long runs = (chunks_per_row + want - 1) / want;
+        return (int)((chunks_per_row + runs - 1) / runs);
+    };
+    P.runA = P.K > 0 ? run_len(P.K, (long)P.B * P.NR, kMaxRunA) : 1;
+    P.RPR = P.K > 0 ? (P.K + P.runA - 1) / P.runA : 0;
+    P.runB = run_len(P.nBi, P.B, kMaxRunB);
+    P.nA = P.NR * P.RPR;
+    P.nph[IT_A] = P.nA;
+    P.nph[IT_D] = P.sample_mode ? 0 : 1;
+    P.nph[IT_B] = (P.nBi + P.runB - 1) / P.runB;
+    P.nph[IT_L] = 1;
+    const long seg = (long)P.nph[0] + P.nph[1] + P.nph[2] + P.nph[3];
+    P.n_items = (unsigned)((long)P.B * seg);
+    const long g = std::min<long>(grid, std::max<long>(1, P.n_items));
+    // Items a CTA may hold: the run in its ring and the one claimed ahead.
+    // Lag between the phases of one batch row, in segments, so a phase's
+    // dependency has completed when a producer reaches it.
+    const long inflight = g * 3;
+    P.claim = 1;
+    P.lag = (int)std::max<long>(1, std::min<long>(P.B, (inflight + seg - 1) / seg + 1));
+    int o = 0;
+    for (int p = 0; p < 4; ++p) {
+        P.off[p] = o;
+        if (P.nph[p] > 0) o += P.lag;
+    }
+    int pts[10], n = 0;
+    pts[n++] = 0;
+    const int tend = P.B + P.off[3];
+    pts[n++] = tend;
+    for (int p = 0; p < 4; ++p) {
+        if (P.nph[p] == 0) continue;
+        pts[n++] = std::min(P.off[p], tend);
+        pts[n++] = std::min(P.off[p] + P.B, tend);
+    }
+    for (int i = 1; i < n; ++i)  // insertion sort of <= 10 points
+        for (int j = i; j > 0 && pts[j - 1] > pts[j]; --j) std::swap(pts[j - 1], pts[j]);
+    P.nbp = 0;
+    for (int i = 0; i < n; ++i)
+        if (P.nbp == 0 || pts[i] != P.bp[P.nbp - 1]) P.bp[P.nbp++] = pts[i];
 }
 
-int stats_chunks(int dtype, const StepParams& P) {
-    int CH = 0;
-    if (dtype == DT_F32) stats_nv_for<float>(P, CH);
-    else if (dtype == DT_BF16) stats_nv_for<__nv_bfloat16>(P, CH);
-    else stats_nv_for<double>(P, CH);
-    return (P.V + CH - 1) / CH;
-}
+int verify_grid(const StepParams& P) { return (int)std::min<long>(2L * sm_count(), std::max<long>(1, P.n_items)); }
 
 template <typename T, int ACT>
-static void launch_pass_t(const StepParams& P, const Launch& L) {
-    dim3 grid((unsigned)((P.NG + kWarps - 1) / kWarps), (unsigned)P.B);
-    const int h = L.begin(KID_ROW_PASS);
-    k_row_pass<T, ACT><<<grid, kThreads, 0, L.st>>>(P);
+static void launch_verify_t(const StepParams& P, const Launch& L) {
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_verify<T, ACT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kVerifySmem);
+        attr = true;
+    }
+    const int grid = (int)std::min<long>(2L * sm_count(), std::max<long>(1, P.n_items));
+    const int h = L.begin(KID_VERIFY);
+    k_verify<T, ACT><<<grid, kBlock, kVerifySmem, L.st>>>(P);
     L.end(h);
 }
 
@@ -866,33 +1233,30 @@ static void launch_mat_t(const StepParams& P, void* p, void* q, void* r, const L
 }
 
 template <typename T>
-static void dispatch_verify(int act, StepParams P, void* outp, void* outq, void* outr, const Launch& L) {
+static void dispatch_verify(int act, const StepParams& P, void* outp, void* outq, void* outr, const Launch& L) {
     const bool mat = outp || outq || outr;
     if (act == ACT_SOFTMAX) {
-        launch_stats_t<T>(P, L);
-        launch_pass_t<T, ACT_SOFTMAX>(P, L);
+        launch_verify_t<T, ACT_SOFTMAX>(P, L);
         if (mat) launch_mat_t<T, ACT_SOFTMAX>(P, outp, outq, outr, L);
     } else if (act == ACT_SIGMOID) {
-        launch_pass_t<T, ACT_SIGMOID>(P, L);
+        launch_verify_t<T, ACT_SIGMOID>(P, L);
         if (mat) launch_mat_t<T, ACT_SIGMOID>(P, outp, outq, outr, L);
     } else {
-        launch_pass_t<T, ACT_PROBS>(P, L);
+        launch_verify_t<T, ACT_PROBS>(P, L);
         if (mat) launch_mat_t<T, ACT_PROBS>(P, outp, outq, outr, L);
     }
 }
 
 void launch_verify(int dtype, int act, const StepParams& P, void* outp, void* outq, void* outr, const Launch& L) {
-    StepParams Q = P;
-    if (act == ACT_SOFTMAX) Q.K = stats_chunks(dtype, P);
-    if (dtype == DT_F32) dispatch_verify<float>(act, Q, outp, outq, outr, L);
-    else if (dtype == DT_BF16) dispatch_verify<__nv_bfloat16>(act, Q, outp, outq, outr, L);
-    else dispatch_verify<double>(act, Q, outp, outq, outr, L);
+    if (dtype == DT_F32) dispatch_verify<float>(act, P, outp, outq, outr, L);
+    else if (dtype == DT_BF16) dispatch_verify<__nv_bfloat16>(act, P, outp, outq, outr, L);
+    else dispatch_verify<double>(act, P, outp, outq, outr, L);
 }
 
 void launch_sample_softmax(int dtype, const StepParams& P, const Launch& L) {
-    if (dtype == DT_F32) launch_pass_t<float, ACT_SOFTMAX>(P, L);
-    else if (dtype == DT_BF16) launch_pass_t<__nv_bfloat16, ACT_SOFTMAX>(P, L);
-    else launch_pass_t<double, ACT_SOFTMAX>(P, L);
+    if (dtype == DT_F32) launch_verify_t<float, ACT_SOFTMAX>(P, L);
+    else if (dtype == DT_BF16) launch_verify_t<__nv_bfloat16, ACT_SOFTMAX>(P, L);
+    else launch_verify_t<double, ACT_SOFTMAX>(P, L);
 }
 
 void launch_gen_logits(int dtype, uint64_t seed, int B, int G, int V, void* zp, void* zq, const Launch& L) {

@@ -14,8 +14,15 @@ enum DType : int { DT_F32 = SSV_F32, DT_BF16 = SSV_BF16, DT_F64 = SSV_F64 };
 enum Act : int { ACT_SOFTMAX = 0, ACT_SIGMOID = 1, ACT_PROBS = 2 };
 enum Mode : int { MODE_NONE = 0, MODE_REJECT = 1, MODE_BONUS = 2 };
 
-// Elements per K2 granule (one warp); the inverse-CDF's first level.
-constexpr int kGranule = 512;
+// Persistent-kernel geometry: a ring of kStages shared-memory stages of
+// kStageBytes each, filled by TMA bulk copies.  A-items (row statistics) take
+// one chunk of kStageBytes; B-items (the rejected pair / bonus row) take half a
+// stage per row; one consumer warp owns one granule (B-item / 8) of a B-item.
+constexpr int kStages = 4;
+constexpr int kStageBytes = 16384;
+constexpr int kStageStride = kStageBytes + 64;  // room for the 16-byte-aligned superset
+constexpr int kHalfStride = kStageStride / 2;   // 16-byte aligned
+constexpr int kLocCap = 1024;                   // granule partials cached in SMEM by locate
 
 // What batch row b still needs after the acceptance scan (K1 -> K2).
 struct Decision {
@@ -31,18 +38,33 @@ struct StepParams {
     const int32_t* ids;
     const double* u;
     int B, G, V, PS;  // batch, gamma, vocab, p steps (gamma or gamma+1)
-    int NR, K, CH;    // K1: stat rows per batch row, chunks per row, chunk elements
-    int NG;           // K2: granules per row
+    int NR, K, CH;    // stat rows per batch row, A-chunks per row, A-chunk elements
+    int NG;           // granules per row
+    int CB, GW;       // B-item elements per row, granule elements (CB / 8)
+    int nA, nBi, lag; // per batch row: A-items, B-items; lag = segments between a row's A- and D-items
+    int nph[4];       // items per batch row of each phase (A, D, B, L)
+    int off[4];       // segment offset of each phase
+    int bp[9], nbp;   // sorted segment breakpoints (piecewise-constant segment sizes)
+    int claim;        // items claimed per atomic by a producer
+    int runA, RPR;    // chunks per A-run, A-runs (= partials) per stat row
+    int runB;         // slices per B-run
+    unsigned long long* trace;  // diagnostics: [2*grid] CTA start/end, [4*B] decide/locate start/end
+    unsigned n_items;
+    unsigned epoch;   // per-launch tag of the decision flags (never reset)
     double alpha, width;
     int sample_mode;    // K2 only: sample softmax(z_p row b) with u[b] (draft sampling)
     int check_uniforms; // StepInputs::validate checks u in [0,1); the sigmoid variant does not
     // scratch
-    double2* part;     // [B][NR][K]  K1 chunk partials (max, sum e^(x-max))
+    double2* part;     // [B][NR][RPR] run partials (max, sum e^(x-max))
     double2* rowstat;  // [B][NR]     row (max, sum)
     Decision* dec;     // [B]
-    double2* gpart;    // [B][NG]     K2 granule partials
-    unsigned* cnt1;    // [B] self-resetting completion counters
-    unsigned* cnt2;    // [B]
+    double2* gpart;    // [B][NG]     granule partials
+    double* gat;       // [B][NR]     logit at the drafted token of each stat row
+    unsigned* cnt1;    // [B] self-resetting completion counters (A-items)
+    unsigned* cnt2;    // [B]                                      (B-items)
+    unsigned* flag;    // [B] decision published (== epoch)
+    unsigned* next;    // [1] work counter, reset by the last CTA to exit
+    unsigned* exit_cnt;// [1]
     // outputs
     int32_t* acc;
     int32_t* fin;
@@ -53,7 +75,7 @@ struct StepParams {
 };
 
 // Kernel ids for the profiling hook (ssv_profile_*).
-enum KernelId : int { KID_ROW_STATS = 0, KID_ROW_PASS = 1, KID_MATERIALIZE = 2, KID_GEN = 3, KID_COUNT = 4 };
+enum KernelId : int { KID_VERIFY = 0, KID_MATERIALIZE = 2, KID_GEN = 3, KID_COUNT = 4 };
 
 // Optional per-launch CUDA-event bracketing (works inside stream capture: the
 // records become graph event nodes).  Owned by the context.
@@ -73,16 +95,17 @@ struct Launch {
         if (!prof || prof->used >= prof->capacity) return -1;
         const int i = prof->used++;
         prof->kid[i] = id;
-        cudaEventRecord(prof->ev[2 * i], st);
+        cudaEventRecordWithFlags(prof->ev[2 * i], st, cudaEventRecordExternal);
         return i;
     }
     void end(int i) const {
         ++*launches;
-        if (i >= 0) cudaEventRecord(prof->ev[2 * i + 1], st);
+        if (i >= 0) cudaEventRecordWithFlags(prof->ev[2 * i + 1], st, cudaEventRecordExternal);
     }
 };
 
-int stats_chunks(int dtype, const StepParams& P);
+void plan_geometry(int dtype, int act, StepParams& P);
+int verify_grid(const StepParams& P);
 void launch_verify(int dtype, int act, const StepParams& P, void* outp, void* outq, void* outr,
                    const Launch& L);
 void launch_sample_softmax(int dtype, const StepParams& P, const Launch& L);

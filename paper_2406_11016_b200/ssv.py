@@ -101,6 +101,7 @@ def load_library() -> C.CDLL:
         L.ssv_profile_disable.argtypes = [vp]
         L.ssv_profile_reset.argtypes = [vp]
         L.ssv_profile_read.argtypes = [vp, i32, C.POINTER(C.c_double), C.POINTER(i32)]
+        L.ssv_debug_trace.argtypes = [vp, C.c_int, vp, vp]
         _lib = L
         return L
 
@@ -112,9 +113,10 @@ EXPORTS = (
     "ssv_verify_probs", "ssv_verify_exact_host", "ssv_verify_sigmoid_host", "ssv_verify_probs_host",
     "ssv_host_alloc", "ssv_host_free", "ssv_sample_softmax", "ssv_make_bench_inputs",
     "ssv_profile_enable", "ssv_profile_disable", "ssv_profile_reset", "ssv_profile_read",
+    "ssv_debug_trace",
 )
 
-KID_ROW_STATS, KID_ROW_PASS, KID_MATERIALIZE, KID_GEN = 0, 1, 2, 3
+KID_VERIFY, KID_MATERIALIZE, KID_GEN = 0, 2, 3
 
 
 @dataclass
@@ -163,6 +165,11 @@ class Verifier:
             raise SsvError(f"ssv_create(device={device}) failed with code {rc} (no CUDA device?)")
         self.ctx = h
         self.device = device
+        self._own_stream = self.lib.ssv_get_stream(h)
+        # Device entry points follow torch's current stream (so they order with
+        # the torch ops that produce their inputs and read their outputs)
+        # unless a stream is pinned with set_stream().
+        self._follow_torch = stream is None
         if stream is not None:
             self.set_stream(stream)
 
@@ -178,9 +185,19 @@ class Verifier:
             pass
 
     def set_stream(self, stream) -> None:
-        """Bind to a torch.cuda.Stream / raw cudaStream_t int (None = own stream)."""
+        """Pin a torch.cuda.Stream / raw cudaStream_t int; None = follow torch's current stream."""
+        if stream is None:
+            self._follow_torch = True
+            return
+        self._follow_torch = False
         handle = getattr(stream, "cuda_stream", stream)
-        self.lib.ssv_set_stream(self.ctx, C.c_void_p(handle) if handle else None)
+        self.lib.ssv_set_stream(self.ctx, C.c_void_p(handle))
+
+    def _bind_torch_stream(self) -> None:
+        if self._follow_torch:
+            import torch
+
+            self.lib.ssv_set_stream(self.ctx, C.c_void_p(torch.cuda.current_stream(self.device).cuda_stream))
 
     @property
     def stream_handle(self) -> int:
@@ -214,10 +231,19 @@ class Verifier:
         self._check(self.lib.ssv_profile_read(self.ctx, kernel_id, C.byref(ms), C.byref(n)), "ssv_profile_read")
         return ms.value, n.value
 
+    def trace_enable(self, capacity: int) -> None:
+        self._check(self.lib.ssv_debug_trace(self.ctx, capacity, None, None), "ssv_debug_trace")
+
+    def trace_read(self, capacity: int):
+        buf = np.zeros(capacity, np.uint64)
+        self._check(self.lib.ssv_debug_trace(self.ctx, capacity, buf.ctypes.data, None), "ssv_debug_trace")
+        return buf
+
     # ---------------- device entry points (torch CUDA tensors) ----------------
     def _device_call(self, fn, what, z_p, z_q, ids, u, alpha, beta, flags, out):
         import torch
 
+        self._bind_torch_stream()
         B, gamma, V = z_q.shape
         a = Args(B, gamma, V, z_p.shape[1], _dtype_code(z_q.dtype), z_p.data_ptr(), z_q.data_ptr(),
                  ids.data_ptr(), u.data_ptr(), alpha, beta, flags)
@@ -257,6 +283,7 @@ class Verifier:
 
         rows, V = logits.shape[-2] if logits.dim() > 1 else 1, logits.shape[-1]
         rows = logits.numel() // V
+        self._bind_torch_stream()
         if out is None:
             out = torch.empty(rows, dtype=torch.int32, device=logits.device)
         rc = self.lib.ssv_sample_softmax(self.ctx, _dtype_code(logits.dtype), logits.data_ptr(), rows, V,
@@ -269,6 +296,7 @@ class Verifier:
         import torch
 
         dev = torch.device("cuda", self.device)
+        self._bind_torch_stream()
         zp = torch.empty(B, gamma + 1, V, dtype=dtype, device=dev)
         zq = torch.empty(B, gamma, V, dtype=dtype, device=dev)
         ids = torch.empty(B, gamma, dtype=torch.int32, device=dev)
@@ -280,6 +308,8 @@ class Verifier:
 
     # ---------------- host entry points (numpy arrays) ----------------
     def _host_call(self, fn, what, z_p, z_q, ids, u, alpha, beta, flags, out, dtype=None):
+        if self._follow_torch:
+            self.lib.ssv_set_stream(self.ctx, C.c_void_p(self._own_stream))  # host entry points sync their own stream
         z_p = np.ascontiguousarray(z_p)
         z_q = np.ascontiguousarray(z_q)
         ids = np.ascontiguousarray(ids, dtype=np.int32)

@@ -74,7 +74,9 @@ def compare(o, g, zp, zq, ids, u, kind, alpha=-1e3, beta=1e3, label=""):
             explained += 1
             continue
         assert g.resample_used[b] == o.resample_used[b], f"{label}: b={b} resample_used"
-        assert abs(g.residual_denom[b] - o.residual_denom[b]) <= DENOM_TOL, (
+        # 1e-6 absolute (results_match), relative for denominators above 1
+        # (sigmoid rows of unnormalized activations reach ~V/2).
+        assert abs(g.residual_denom[b] - o.residual_denom[b]) <= DENOM_TOL * max(1.0, abs(o.residual_denom[b])), (
             f"{label}: b={b} residual_denom {g.residual_denom[b]} vs {o.residual_denom[b]}")
         if g.final_token[b] != o.final_token[b]:
             a = int(o.accepted_len[b])

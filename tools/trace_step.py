@@ -1,0 +1,50 @@
+"""Phase timeline of one verify launch (globaltimer trace; diagnostics only)."""
+import argparse
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+from paper_2406_11016_b200 import Verifier  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--B", type=int, default=8)
+ap.add_argument("--gamma", type=int, default=5)
+ap.add_argument("--V", type=int, default=51865)
+ap.add_argument("--dtype", default="f32")
+ap.add_argument("--variant", default="exact")
+a = ap.parse_args()
+v = Verifier(0)
+dt = {"f32": torch.float32, "bf16": torch.bfloat16}[a.dtype]
+zp, zq, ids, u = v.make_bench_inputs(1, a.B, a.gamma, a.V, dt)
+run = (lambda: v.verify_exact(zp, zq, ids, u)) if a.variant == "exact" else (lambda: v.verify_sigmoid(zp, zq, ids, u))
+for _ in range(3):
+    run()
+torch.cuda.synchronize()
+cap = 2 * 296 + 4 * a.B
+v.trace_enable(cap)
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+s = torch.cuda.Stream()
+v.set_stream(s)
+with torch.cuda.stream(s):
+    e0.record(s)
+    r = run()
+    e1.record(s)
+s.synchronize()
+t = v.trace_read(cap).astype(np.int64)
+grid = 296
+cta = t[: 2 * grid].reshape(grid, 2)
+cta = cta[cta[:, 0] > 0]
+t0 = cta[:, 0].min()
+print(f"event ms {e0.elapsed_time(e1) * 1e3:.1f} us; kernel span {(cta[:, 1].max() - t0) / 1e3:.1f} us; "
+      f"CTA start spread {(cta[:, 0].max() - t0) / 1e3:.1f} us; CTA end min {(cta[:, 1].min() - t0) / 1e3:.1f} us")
+ph = t[2 * grid: 2 * grid + 4 * a.B].reshape(a.B, 4)
+acc = r.accepted_len.cpu().numpy()
+for b in range(min(a.B, 16)):
+    f = lambda x: f"{(x - t0) / 1e3:7.1f}" if x > 0 else "      -"
+    print(f"b={b:3d} acc={acc[b]} D {f(ph[b, 0])} -> {f(ph[b, 1])}   L {f(ph[b, 2])} -> {f(ph[b, 3])}")
+if a.B > 16:
+    valid = ph[:, 0] > 0
+    print("D start max", (ph[valid, 0].max() - t0) / 1e3, "L end max", (ph[ph[:, 3] > 0, 3].max() - t0) / 1e3)
