@@ -25,9 +25,8 @@ struct ssv_ctx {
     // stream-ordered scratch
     void* scratch = nullptr;
     size_t scratch_bytes = 0;
-    unsigned* counters = nullptr;  // [2 + 3 * counters_n]: next, exit, cnt1[n], cnt2[n], flag[n]
+    unsigned* counters = nullptr;  // [2 + 3 * counters_n]: next, exit, cnt1[n], cnt2[n], flag[n] (kernels leave them 0)
     size_t counters_n = 0;
-    unsigned epoch = 0;            // decision-flag tag, one per launch
     uint32_t* status_dev = nullptr;  // default status word
     // host-entry staging
     void* stage = nullptr;
@@ -122,28 +121,25 @@ int ensure_scratch(ssv_ctx* ctx, size_t bytes, size_t counters_n) {
         CK(cudaMalloc(&ctx->counters, (2 + 3 * nn) * sizeof(unsigned)));
         CK(cudaMemset(ctx->counters, 0, (2 + 3 * nn) * sizeof(unsigned)));
         ctx->counters_n = nn;
-        ctx->epoch = 0;
     }
     return SSV_OK;
 }
 
 struct Layout {
-    size_t part, rowstat, dec, gpart, gat, extra, total;
+    size_t part, rowstat, dec, gpart, extra, total;
 };
 
 Layout plan_scratch(const StepParams& P, size_t extra_bytes) {
     Layout L;
     size_t off = 0;
     L.part = off;
-    off = align_up(off + (size_t)P.B * P.NR * std::max(P.RPR, 1) * sizeof(double2));
+    off = align_up(off + (size_t)P.B * std::max(P.NR, 1) * std::max(P.K, 1) * kWarpsPerCta * sizeof(double2));
     L.rowstat = off;
     off = align_up(off + (size_t)P.B * std::max(P.NR, 1) * sizeof(double2));
     L.dec = off;
     off = align_up(off + (size_t)P.B * sizeof(Decision));
     L.gpart = off;
     off = align_up(off + (size_t)P.B * P.NG * sizeof(double2));
-    L.gat = off;
-    off = align_up(off + (size_t)P.B * std::max(P.NR, 1) * sizeof(double));
     L.extra = off;
     off = align_up(off + extra_bytes);
     L.total = off;
@@ -156,14 +152,11 @@ void bind_scratch(ssv_ctx* ctx, StepParams& P, const Layout& L) {
     P.rowstat = reinterpret_cast<double2*>(s + L.rowstat);
     P.dec = reinterpret_cast<Decision*>(s + L.dec);
     P.gpart = reinterpret_cast<double2*>(s + L.gpart);
-    P.gat = reinterpret_cast<double*>(s + L.gat);
     P.next = ctx->counters;
     P.exit_cnt = ctx->counters + 1;
     P.cnt1 = ctx->counters + 2;
     P.cnt2 = P.cnt1 + ctx->counters_n;
     P.flag = P.cnt2 + ctx->counters_n;
-    P.epoch = ++ctx->epoch;
-    if (P.epoch == 0) P.epoch = ++ctx->epoch;  // flags start at 0: never reuse it
 }
 
 int run_device(ssv_ctx* ctx, int variant, const ssv_verify_args* a, ssv_verify_out* o) {
@@ -195,7 +188,7 @@ int run_device(ssv_ctx* ctx, int variant, const ssv_verify_args* a, ssv_verify_o
     P.tau = o->tau;
     P.rden = o->residual_denom;
     P.status = o->status ? o->status : ctx->status_dev;
-    P.trace = (ctx->trace && 3 * verify_grid(P) + 4 * P.B <= ctx->trace_cap) ? ctx->trace : nullptr;
+    P.trace = (ctx->trace && trace_slots(P) <= ctx->trace_cap) ? ctx->trace : nullptr;
     ctx->launches = 0;
     launch_verify(a->dtype, variant, P, want_p ? o->p : nullptr, (a->flags & SSV_WANT_Q) ? o->q : nullptr,
                   (a->flags & SSV_WANT_RESIDUAL) ? o->residual : nullptr, ctx->launcher());
@@ -487,7 +480,7 @@ int ssv_sample_softmax(ssv_ctx* ctx, int32_t dtype, const void* logits, int32_t 
     if (rc) return rc;
     bind_scratch(ctx, P, L);
     P.fin = tokens_out;
-    P.trace = (ctx->trace && 3 * verify_grid(P) + 4 * P.B <= ctx->trace_cap) ? ctx->trace : nullptr;
+    P.trace = (ctx->trace && trace_slots(P) <= ctx->trace_cap) ? ctx->trace : nullptr;
     P.status = status ? status : ctx->status_dev;
     ctx->launches = 0;
     launch_sample_softmax(dtype, P, ctx->launcher());

@@ -122,6 +122,24 @@ __device__ __forceinline__ double exp_neg(double t) { return exp(-t); }
 __device__ __forceinline__ float expm1_acc(float x) { return expm1f(x); }
 __device__ __forceinline__ double expm1_acc(double x) { return expm1(x); }
 
+// ---- sm_100a three-input min/max (FMNMX3) and packed fp32x2 arithmetic ------
+// (FADD2 / FMUL2): the per-element hot ops of the row-statistics pass.
+__device__ __forceinline__ float fmax3f(float a, float b, float c) {
+    float r;
+    asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+    return r;
+}
+__device__ __forceinline__ float fmin3f(float a, float b, float c) {
+    float r;
+    asm("min.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+    return r;
+}
+__device__ __forceinline__ float ex2f(float t) {
+    float r;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(t));
+    return r;
+}
+
 // ---- warp / block reductions (fixed topology) ------------------------------
 template <typename V>
 __device__ __forceinline__ V warp_sum(V v) {

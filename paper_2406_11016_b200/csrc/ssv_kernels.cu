@@ -1,36 +1,39 @@
 // ssv_kernels.cu -- sm_100a kernels of the speculative-sampling verification step.
 //
-// k_verify<T, ACT> is the whole step in ONE persistent, warp-specialized
-// launch (DESIGN.md has the derivation and the roofline):
+// k_verify<T, ACT> is the whole step in ONE launch of independent work items,
+// one 256-thread CTA each, ordered so every wait is on an item with a smaller
+// block index (DESIGN.md has the derivation and the roofline):
 //
-//   producer warp   claims work items in order from a global counter and
-//                   streams their bytes into a kStages-deep ring of shared-
-//                   memory stages with TMA bulk copies (cp.async.bulk, 16-byte
-//                   aligned supersets of misaligned rows) completing on mbarriers.
-//   consumer warps  (8) drain the ring:
-//     A-item  (exact only) one chunk of one drafted p/q row: CTA max, fp32 ex2
-//             sums with fp64 carries -> chunk partial (m, s); the logit at the
-//             drafted token is picked out of the stage.  The consumer group
-//             that completes batch row b's LAST A-item folds the partials into
-//             row statistics, evaluates tau at every drafted position in fp64,
-//             runs the first-rejection scan and publishes the decision
-//             (release flag, tagged with the launch epoch).
-//     D-item  (sigmoid / probabilities) the same decision from the B*gamma
-//             gathered logits alone -- no row reductions (paper section 3.2.2).
-//     B-item  one slice of the ONE row (bonus) or row PAIR (rejected position)
-//             batch row b still needs; the producer waits for b's decision
-//             before fetching it.  Each consumer warp reduces one granule to
-//             its residual mass max(0, p - q) (or p mass / (m, s) for the bonus
-//             row).  B-items of b are ordered after the A-items of b + lag, so
-//             the rejected pair is re-read from L2, not HBM.
-//             The group completing b's LAST B-item runs the inverse CDF: fp64
-//             granule prefix from SMEM, then an exact fp64 scan inside the
-//             selected granule (dist.cpp:122-137, incl. its fallbacks).
+//   A-item  (exact only) a 16-byte-aligned chunk of one drafted p / q row,
+//           4 KB * nv of it, loaded straight into registers with 128-bit
+//           streaming loads (nv loads in flight per thread).  CTA max with
+//           FMNMX3, then e^(x - max) with packed FADD2/FMUL2 + MUFU ex2 summed in
+//           fp32 pairs, fp64 across threads -> one partial (max, sum).
+//           The CTA that completes batch row b's LAST A-item folds the
+//           partials into row statistics, evaluates tau at every drafted
+//           position in fp64 (activation.cpp:20-27 + verify_reference.cpp:
+//           87-92), runs the first-rejection scan (93-96) and publishes the
+//           decision (release flag).
+//   B-item  kCB elements of the ONE row (bonus) or row PAIR (rejected
+//           position) batch row b still needs; each warp reduces one granule
+//           to its residual mass max(0, p - q) (or p mass / (m, s) for the
+//           bonus row).  Exact: the item waits for b's decision, which its
+//           position in the grid (after the A-items of b + lag) makes ready,
+//           and it re-reads the rejected pair from L2, not HBM.  Sigmoid /
+//           probabilities: the item takes the decision itself from the B*gamma
+//           gathered values (paper section 3.2.2) -- no row reductions, no wait.
+//           The CTA completing b's LAST B-item runs the inverse CDF: fp64
+//           granule prefix, then an exact fp64 scan inside the selected granule
+//           (dist.cpp:122-137, incl. its fallbacks), and resets b's counters.
 //
-// Every reduction has a fixed topology, so results are bit-identical run to
-// run.  k_materialize (optional p / q / residual grids) and the synthetic-input
-// generator follow.
+// Items are dispatched in block-index order (the in-order CTA rasterization
+// single-pass scans rely on), so a waiting B-item's A-items are all resident
+// or retired: no deadlock, no persistent scheduler.  Every reduction has a
+// fixed topology, so results are bit-identical run to run.  k_materialize
+// (optional p / q / residual grids) and the synthetic-input generator follow.
 #include <algorithm>
+#include <cfloat>
+#include <cstdlib>
 #include <type_traits>
 
 #include "ssv_launch.h"
@@ -39,48 +42,19 @@
 
 namespace ssv {
 
-constexpr int kCons = 256;                 // consumer threads (8 warps)
-constexpr int kConsWarps = kCons / 32;
-constexpr int kBlock = kCons + 32;         // + one producer warp
-
-// Work-item phases of one batch row, in dependency order.
-enum ItemType : int { IT_A = 0, IT_D = 1, IT_B = 2, IT_L = 3, IT_STOP = 4 };
 constexpr int kMaxRowsSmem = 96;  // row statistics a decide keeps in SMEM (gamma <= 47)
+constexpr int kCtaMinBlocks = 3;  // resident CTAs per SM (64 KB ring each)
+static_assert(kLocCap * sizeof(double2) <= (size_t)kDynSmem, "granule cache aliases the ring");
 
-constexpr int kMaxRunA = 64;  // chunks per A-run (row-statistics run)
-constexpr int kMaxRunB = 8;   // slices per B-run (residual / bonus run)
-constexpr int kCtx = 8;       // run contexts (runs in flight per CTA; see RunInfo)
-
-// Work-item description handed from producer to consumers.  A- and B-items
-// are RUNS of consecutive chunks of one row; a run is streamed one 16 KB chunk
-// per ring stage.
-struct Item {
-    int type, b;
-    int r, q;            // A: stat row, run index within the row; B: run index
-    int mode, row;       // B / L: decision
-    double Mp, Sp, Mq, Sq;
-};
-
-// One ring slot (16 bytes for A/B chunks; D/L items also carry the decision).
-struct Slot {
-    int type, ctx, pos, b;
-    int mode, row, pad0, pad1;
-    double Mp, Sp, Mq, Sq;
-};
-
-// Per-run constants (written once by the producer before the run's first
-// chunk is published) and the consumers' fold state.  kCtx contexts: consumer
-// warps can be at most kStages chunks apart (a stage is refilled only after
-// all 8 warps released it), so a context is free again long before the
-// producer reuses it kCtx runs later.
-struct RunInfo {
-    int type, b, r, q, len, k0;  // k0: first chunk (A) / slice (B) of the run
-    int mode, row, shift_p, shift_q;
-    double Mp, Sp, Mq, Sq;
-    double2 wpart[kConsWarps];   // A: warp partials (max, sum) of the run
-    double wmin[kConsWarps];
-    double2 gpart[kMaxRunB * kConsWarps];  // B: granule partials of the run
-    unsigned cnt;                // warps done with the run
+struct Shared {
+    float fred[kWarps];
+    double dred[kWarps];
+    int ired[kWarps];
+    int last;
+    unsigned item, item_next;
+    Decision dec;
+    double2 wpart[kWarps];
+    double2 rs[kMaxRowsSmem];
 };
 
 // ---------------------------------------------------------------------------
@@ -108,7 +82,6 @@ __device__ __forceinline__ unsigned long long gtime() {
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     return t;
 }
-// Diagnostics: phase timestamps (ns) when a trace buffer is attached.
 __device__ __forceinline__ void trace(const StepParams& P, int idx) {
     if (P.trace) P.trace[idx] = gtime();
 }
@@ -118,276 +91,307 @@ __device__ __forceinline__ double ratio_clamped(double p, double q) {  // dist.c
     return fmin(1.0, p / q);
 }
 
-// ---- consumer-group collectives (named barrier 1, 256 threads) -------------
-template <typename V, typename Op>
-__device__ __forceinline__ V creduce(V v, V* sm, Op op) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v = op(v, __shfl_xor_sync(kFull, v, o));
-    cbar<kCons>();
-    if (lane == 0) sm[warp] = v;
-    cbar<kCons>();
-    V r = sm[0];
-#pragma unroll
-    for (int w = 1; w < kConsWarps; ++w) r = op(r, sm[w]);
-    return r;
-}
-
-__device__ __forceinline__ double cscan_incl(double v, double* sm, double& total) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const double incl = warp_scan_incl(v);
-    cbar<kCons>();
-    if (lane == 31) sm[warp] = incl;
-    cbar<kCons>();
-    double off = 0.0, tot = 0.0;
-#pragma unroll
-    for (int w = 0; w < kConsWarps; ++w) {
-        if (w < warp) off += sm[w];
-        tot += sm[w];
-    }
-    total = tot;
-    return off + incl;
-}
-
-template <typename T>
-__device__ __forceinline__ typename Elem<T>::acc lds_elem(const uint8_t* base, int i) {
-    return (typename Elem<T>::acc)load_smem_elem(reinterpret_cast<const T*>(base) + i);
-}
-
 // ---------------------------------------------------------------------------
-// Work-item order.  Segment t holds, in order, the A-items of batch row t,
-// the decide item of t - off[1], the B-items of t - off[2] and the locate item
-// of t - off[3] (each only if that row exists).  Items only ever wait on items
-// with a smaller index -- claimed earlier by a running CTA -- so the schedule
-// cannot deadlock, and the lags keep the waits short and the rejected pair of
-// row b L2-resident when its B-items stream it again.
-__device__ __forceinline__ int seg_size(const StepParams& P, int t) {
-    int n = 0;
+// Item order.  Segment t holds, in order, the A-items of batch row t - off[A],
+// the D-item of t - off[D], the B-items of t - off[B] and the L-item of
+// t - off[L] (each only if that row exists and the phase has items).  Every
+// item waits only on items of an earlier phase of the same row, i.e. on
+// smaller block indices.  The segment composition is piecewise constant over
+// at most 8 ranges the host tabulates.
+enum ItemType : int { IT_A = 0, IT_D = 1, IT_B = 2, IT_L = 3 };
+struct ItemRef {
+    int type, b, idx;
+};
+
+__device__ __forceinline__ ItemRef decode_item(const StepParams& P, unsigned i) {
+    int k = 0;
+    while (k + 1 < P.nrange && i >= P.ritem[k + 1]) ++k;
+    const unsigned rel = i - P.ritem[k], sz = (unsigned)P.rsize[k];
+    const int t = P.rseg[k] + (int)(rel / sz);
+    int o = (int)(rel % sz);
 #pragma unroll
     for (int p = 0; p < 4; ++p) {
         const int b = t - P.off[p];
-        if (b >= 0 && b < P.B) n += P.nph[p];
-    }
-    return n;
-}
-
-// Position of an item: segment t, phase p, index a within the phase.
-struct Cursor {
-    int t, p, a;
-};
-
-__device__ __forceinline__ bool phase_active(const StepParams& P, int t, int p) {
-    const int b = t - P.off[p];
-    return P.nph[p] > 0 && b >= 0 && b < P.B;
-}
-
-// First active phase of segment t at or after phase p (p may be 4: next segment).
-__device__ __forceinline__ void settle(const StepParams& P, Cursor& c) {
-    const int tend = P.B + P.off[3];
-    while (c.t < tend) {
-        while (c.p < 4 && !phase_active(P, c.t, c.p)) ++c.p;
-        if (c.p < 4) return;
-        ++c.t;
-        c.p = 0;
-        c.a = 0;
-    }
-}
-
-__device__ __forceinline__ Cursor decode_cursor(const StepParams& P, unsigned i) {
-    Cursor c{P.B + P.off[3], 0, 0};  // past the end
-    if (i >= P.n_items) return c;
-    unsigned cum = 0;
-    int o = 0;
-    for (int q = 0; q + 1 < P.nbp; ++q) {
-        const int x = P.bp[q], y = P.bp[q + 1];
-        const int sz = seg_size(P, x);
-        const unsigned cnt = (unsigned)(y - x) * (unsigned)sz;
-        if (sz > 0 && i < cum + cnt) {
-            c.t = x + (int)((i - cum) / (unsigned)sz);
-            o = (int)((i - cum) % (unsigned)sz);
-            break;
-        }
-        cum += cnt;
-    }
-    c.p = 0;
-    c.a = 0;
-    for (int p = 0; p < 4; ++p) {
-        if (!phase_active(P, c.t, p)) continue;
-        if (o < P.nph[p]) {
-            c.p = p;
-            c.a = o;
-            return c;
-        }
+        if (P.nph[p] == 0 || b < 0 || b >= P.B) continue;
+        if (o < P.nph[p]) return {p, b, o};
         o -= P.nph[p];
     }
-    return c;
+    return {IT_L, 0, 0};  // unreachable
 }
 
-__device__ __forceinline__ void advance(const StepParams& P, Cursor& c) {
-    if (++c.a < P.nph[c.p]) return;
-    c.a = 0;
-    ++c.p;
-    settle(P, c);
+__device__ __forceinline__ void red_release_add(unsigned* p, unsigned v) {
+    asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
-__device__ __forceinline__ void cursor_item(const StepParams& P, const Cursor& c, Item& it) {
-    it.type = IT_STOP;
-    if (c.t >= P.B + P.off[3]) return;
-    it.type = c.p;
-    it.b = c.t - P.off[c.p];
-    if (c.p == IT_A) {
-        it.r = c.a / P.RPR;
-        it.q = c.a - it.r * P.RPR;
-    } else {
-        it.q = c.a;
-    }
-}
-
-// Bulk-copy the 16-byte-aligned superset of [lo, hi) of `row` into dst;
-// returns the copied bytes and the element shift of `lo` inside it.
-template <typename T>
-__device__ __forceinline__ uint32_t stage_range(const T* row, int lo, int hi, uint8_t* dst, uint64_t* bar,
-                                                int& shift) {
-    const uintptr_t a0 = reinterpret_cast<uintptr_t>(row + lo);
-    const uintptr_t a1 = reinterpret_cast<uintptr_t>(row + hi);
-    const uintptr_t s0 = a0 & ~uintptr_t(15), s1 = (a1 + 15) & ~uintptr_t(15);
-    shift = (int)((a0 - s0) / sizeof(T));
-    const uint32_t bytes = (uint32_t)(s1 - s0);
-    bulk_g2s(dst, reinterpret_cast<const void*>(s0), bytes, bar);
-    return bytes;
-}
-
-template <typename T>
-__device__ __forceinline__ uint32_t staged_bytes(const T* row, int lo, int hi) {
-    const uintptr_t a0 = reinterpret_cast<uintptr_t>(row + lo);
-    const uintptr_t a1 = reinterpret_cast<uintptr_t>(row + hi);
-    return (uint32_t)(((a1 + 15) & ~uintptr_t(15)) - (a0 & ~uintptr_t(15)));
+__device__ __forceinline__ void wait_geq(const unsigned* p, unsigned v) {
+    while (ld_acquire(p) < v) __nanosleep(40);
 }
 
 // ---------------------------------------------------------------------------
-// Producer: lane 0 of the last warp.  Claims kClaim items per atomic, waits
-// for an item's dependencies (acquire loads of the completion counters and the
-// decision flag), then fills the next ring stage: TMA bulk copies for A- and
-// B-items, a bare arrive for decide / locate items.
-__device__ __forceinline__ void wait_eq(const unsigned* p, unsigned v) {
-    while (ld_acquire(p) != v) __nanosleep(32);
+// A-item helpers.  Elements outside the row inside an edge vector are padded
+// with -max (finite: neutral for the max, e^(pad - max) = 0, and invisible to
+// the -inf check).
+template <typename T>
+__device__ __forceinline__ uint4 pad_vec();
+template <>
+__device__ __forceinline__ uint4 pad_vec<float>() { return make_uint4(0xff7fffffu, 0xff7fffffu, 0xff7fffffu, 0xff7fffffu); }
+template <>
+__device__ __forceinline__ uint4 pad_vec<__nv_bfloat16>() {
+    return make_uint4(0xff7fff7fu, 0xff7fff7fu, 0xff7fff7fu, 0xff7fff7fu);
 }
+template <>
+__device__ __forceinline__ uint4 pad_vec<double>() { return make_uint4(0xffffffffu, 0xffefffffu, 0xffffffffu, 0xffefffffu); }
 
-__device__ __forceinline__ bool load_decision(const StepParams& P, Item& it) {
-    if (P.sample_mode) {
-        it.mode = MODE_BONUS;
-        it.row = 0;
-        it.Mp = it.Mq = 0.0;
-        it.Sp = it.Sq = 1.0;
-        return true;
-    }
-    wait_eq(&P.flag[it.b], P.epoch);
-    const Decision* d = &P.dec[it.b];
-    it.mode = __ldcg(&d->mode);
-    if (it.mode == MODE_NONE) return false;
-    it.row = __ldcg(&d->row);
-    it.Mp = __ldcg(&d->Mp);
-    it.Sp = __ldcg(&d->Sp);
-    it.Mq = __ldcg(&d->Mq);
-    it.Sq = __ldcg(&d->Sq);
-    return true;
-}
-
-template <typename T, int ACT>
-__device__ void producer(const StepParams& P, uint8_t* stages, uint64_t* full, uint64_t* empty, Slot* slots,
-                         RunInfo* runs) {
-    constexpr int CA = kStageBytes / (int)sizeof(T);
-    unsigned cur = atomicAdd(P.next, 1u);
-    unsigned nxt = atomicAdd(P.next, 1u);  // next item, claimed one ahead
-    if (P.trace) P.trace[2 * gridDim.x + 4 * P.B + blockIdx.x] = cur;
-    unsigned n = 0, runseq = 0;
-    auto stage = [&](unsigned& sidx) -> uint8_t* {
-        const unsigned s = n % kStages, ph = (n / kStages) & 1u;
-        mbar_wait(&empty[s], ph ^ 1u);
-        sidx = s;
-        return stages + (size_t)s * kStageStride;
-    };
-    for (;;) {
-        Item it;
-        cursor_item(P, decode_cursor(P, cur), it);
-        cur = nxt;
-        nxt = atomicAdd(P.next, 1u);
-        if (it.type == IT_D) {
-            if (ACT == ACT_SOFTMAX && !P.sample_mode) wait_eq(&P.cnt1[it.b], (unsigned)P.nph[IT_A]);
-        } else if (it.type == IT_B) {
-            if (!load_decision(P, it)) continue;
-        } else if (it.type == IT_L) {
-            if (!load_decision(P, it)) continue;
-            wait_eq(&P.cnt2[it.b], (unsigned)P.nph[IT_B]);
+// Keep elements [lo, hi) of the vector, pad the rest.
+template <typename T>
+__device__ __forceinline__ void mask_vec(uint4& w, int lo, int hi) {
+    constexpr int VEC = Elem<T>::VEC;
+    constexpr int EPW = VEC / 4 > 0 ? VEC / 4 : 1;  // elements per 32-bit word (1 or 2); fp64: 1/2
+    const uint4 pad = pad_vec<T>();
+    uint32_t* wv = reinterpret_cast<uint32_t*>(&w);
+    const uint32_t* pv = reinterpret_cast<const uint32_t*>(&pad);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        if (sizeof(T) == 8) {
+            const int e = q / 2;
+            if (e < lo || e >= hi) wv[q] = pv[q];
+        } else if (EPW == 1) {
+            if (q < lo || q >= hi) wv[q] = pv[q];
+        } else {
+            const int e0 = 2 * q, e1 = 2 * q + 1;
+            const uint32_t keep = ((e0 >= lo && e0 < hi) ? 0x0000ffffu : 0u) | ((e1 >= lo && e1 < hi) ? 0xffff0000u : 0u);
+            wv[q] = (wv[q] & keep) | (pv[q] & ~keep);
         }
-        if (it.type == IT_A || it.type == IT_B) {
-            const int c = (int)(runseq++ % kCtx);
-            RunInfo& ri = runs[c];
-            const T* pr;
-            const T* qr = nullptr;
-            int k0, k1, step;
-            if (it.type == IT_A) {
-                pr = stat_row<T>(P, it.b, it.r);
-                k0 = it.q * P.runA;
-                k1 = min(k0 + P.runA, P.K);
-                step = CA;
+    }
+}
+
+// Thread partials over the loaded vectors: max / min (pass 1) and
+// sum e^(x - M) (pass 2).  fp32 / bf16: FMNMX3, FADD2/FMUL2, MUFU ex2, fp32
+// pair sums (<= 16 terms each) widened to fp64.  fp64 storage: libdevice exp.
+template <typename T>
+struct AStat;
+
+template <>
+struct AStat<float> {
+    static __device__ __forceinline__ void minmax(const uint4& v, float& m, float& n) {
+        const float a = __uint_as_float(v.x), b = __uint_as_float(v.y), c = __uint_as_float(v.z),
+                    d = __uint_as_float(v.w);
+        m = fmax3f(m, a, b);
+        m = fmax3f(m, c, d);
+        n = fmin3f(n, a, b);
+        n = fmin3f(n, c, d);
+    }
+    static __device__ __forceinline__ void expsum(const uint4& v, float2 negM, float2& s) {
+        const float2 l2e = make_float2(1.4426950408889634f, 1.4426950408889634f);
+        float2 t0 = __fmul2_rn(__fadd2_rn(make_float2(__uint_as_float(v.x), __uint_as_float(v.y)), negM), l2e);
+        float2 t1 = __fmul2_rn(__fadd2_rn(make_float2(__uint_as_float(v.z), __uint_as_float(v.w)), negM), l2e);
+        s = __fadd2_rn(s, make_float2(ex2f(t0.x), ex2f(t0.y)));
+        s = __fadd2_rn(s, make_float2(ex2f(t1.x), ex2f(t1.y)));
+    }
+};
+
+template <>
+struct AStat<__nv_bfloat16> {
+    static __device__ __forceinline__ void minmax(const uint4& v, float& m, float& n) {
+        float x[8];
+        unpack(v, x);
+        m = fmax3f(m, x[0], x[1]);
+        m = fmax3f(m, x[2], x[3]);
+        m = fmax3f(m, x[4], x[5]);
+        m = fmax3f(m, x[6], x[7]);
+        n = fmin3f(n, x[0], x[1]);
+        n = fmin3f(n, x[2], x[3]);
+        n = fmin3f(n, x[4], x[5]);
+        n = fmin3f(n, x[6], x[7]);
+    }
+    static __device__ __forceinline__ void expsum(const uint4& v, float2 negM, float2& s) {
+        const float2 l2e = make_float2(1.4426950408889634f, 1.4426950408889634f);
+        float x[8];
+        unpack(v, x);
+#pragma unroll
+        for (int e = 0; e < 8; e += 2) {
+            const float2 t = __fmul2_rn(__fadd2_rn(make_float2(x[e], x[e + 1]), negM), l2e);
+            s = __fadd2_rn(s, make_float2(ex2f(t.x), ex2f(t.y)));
+        }
+    }
+};
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem)), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+// Geometry of one A-run (a run of chunks of one statistics row).  Chunk c of
+// a row is vectors [c * CV, (c + 1) * CV) of the 16-byte-aligned superset of
+// the row; thread t owns vectors t + 256 j (j < kAVec) of every chunk.
+template <typename T>
+struct ARun {
+    const uint4* vb;  // aligned row base
+    int nvec_row, shift, tail;
+    int c0, n;        // first chunk, chunks in the run
+    __device__ __forceinline__ void init(const StepParams& P, int b, int idx) {
+        constexpr int VEC = Elem<T>::VEC;
+        const int r = idx / P.K, q = idx - r * P.K;
+        const uintptr_t a0 = reinterpret_cast<uintptr_t>(stat_row<T>(P, b, r));
+        shift = (int)((a0 & 15) / sizeof(T));
+        nvec_row = (shift + P.V + VEC - 1) / VEC;
+        tail = (shift + P.V) % VEC;
+        vb = reinterpret_cast<const uint4*>(a0 - (a0 & 15));
+        c0 = q * P.runA;
+        n = min(c0 + P.runA, P.Kc) - c0;
+    }
+    // cp.async this thread's vectors of chunk c0 + k into ring slot `slot`
+    __device__ __forceinline__ void issue(int k, uint4* ring, unsigned slot) const {
+        constexpr int CV = kCtaThreads * kAVec;
+        uint4* st = ring + (size_t)slot * CV;
+#pragma unroll
+        for (int j = 0; j < kAVec; ++j) {
+            const int v = (c0 + k) * CV + threadIdx.x + kCtaThreads * j;
+            if (v < nvec_row) cp_async16(st + j * kCtaThreads + threadIdx.x, vb + v);
+        }
+        cp_async_commit();
+    }
+};
+
+// The CTA's cp.async stream: every issued chunk is one commit group and owns
+// ring slot (position % kAStages); at most kAStages are outstanding.
+struct AStream {
+    unsigned issued = 0, consumed = 0;
+    int next_pre = 0;  // chunks of the NEXT run already issued
+};
+
+__device__ __forceinline__ void cp_async_wait_pending(unsigned n) {  // wait until <= n groups pending
+    switch (n) {
+        case 0: cp_async_wait<0>(); break;
+        case 1: cp_async_wait<1>(); break;
+        case 2: cp_async_wait<2>(); break;
+        default: cp_async_wait<3>(); break;
+    }
+    static_assert(kAStages == 4, "wait switch covers kAStages - 1 pending groups");
+}
+
+// A-item: run q of statistics row r of batch row b.  The run's chunks stream
+// through the ring kAStages - 1 ahead, and its tail already streams the first
+// chunks of the next claimed item when that is an A-run too, so the loads of
+// consecutive runs overlap (no drain / refill per run).  Per thread: running
+// max (fp32) and sum e^(x - max) (fp64, the chunk's 16-32 terms summed in fp32
+// pairs); an fp64 exp only when the max grows.  End of run: warp fold, CTA
+// fold (fixed order) -> one partial.
+template <typename T>
+__device__ void item_A(const StepParams& P, int b, int idx, const ItemRef& nxt, Shared& sh, uint4* ring,
+                       AStream& as) {
+    constexpr int VEC = Elem<T>::VEC;
+    constexpr int CV = kCtaThreads * kAVec;  // vectors per chunk
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int r = idx / P.K, q = idx - r * P.K;
+    ARun<T> cur;
+    cur.init(P, b, idx);
+    ARun<T> nr;
+    const bool pre = nxt.type == IT_A;
+    if (pre) nr.init(P, nxt.b, nxt.idx);
+    int cur_issued = as.next_pre;  // the previous run already issued these
+    int nxt_issued = 0;
+    const int shift = cur.shift, tail = cur.tail, nvec_row = cur.nvec_row;
+    using A = typename Elem<T>::acc;
+    A m = -FLT_MAX, mn = FLT_MAX;
+    if constexpr (sizeof(T) == 8) {
+        m = -DBL_MAX;
+        mn = DBL_MAX;
+    }
+    double s = 0.0;
+    for (int k = 0; k < cur.n; ++k) {
+        while (as.issued - as.consumed < (unsigned)kAStages) {  // top up the ring
+            if (cur_issued < cur.n) {
+                cur.issue(cur_issued++, ring, as.issued % kAStages);
+            } else if (pre && nxt_issued < min(nr.n, kAStages - 1)) {
+                nr.issue(nxt_issued++, ring, as.issued % kAStages);
             } else {
-                pr = p_row<T>(P, it.b, it.row);
-                if (it.mode == MODE_REJECT) qr = q_row<T>(P, it.b, it.row);
-                k0 = it.q * P.runB;
-                k1 = min(k0 + P.runB, P.nBi);
-                step = P.CB;
+                break;
             }
-            // chunk starts are 16 KB / 8 KB apart: the misalignment is constant per row
-            ri.type = it.type;
-            ri.b = it.b;
-            ri.r = it.r;
-            ri.q = it.q;
-            ri.len = k1 - k0;
-            ri.k0 = k0;
-            ri.mode = it.mode;
-            ri.row = it.row;
-            ri.Mp = it.Mp;
-            ri.Sp = it.Sp;
-            ri.Mq = it.Mq;
-            ri.Sq = it.Sq;
-            ri.shift_p = (int)((reinterpret_cast<uintptr_t>(pr + (size_t)k0 * step) & 15) / sizeof(T));
-            ri.shift_q = qr ? (int)((reinterpret_cast<uintptr_t>(qr + (size_t)k0 * step) & 15) / sizeof(T)) : 0;
-            for (int k = k0; k < k1; ++k) {
-                unsigned s;
-                uint8_t* st = stage(s);
-                const int lo = k * step, hi = min(lo + step, P.V);
-                uint32_t bytes = staged_bytes(pr, lo, hi);
-                if (qr) bytes += staged_bytes(qr, lo, hi);
-                slots[s].type = it.type;
-                slots[s].ctx = c;
-                slots[s].pos = k - k0;
-                slots[s].b = it.b;
-                mbar_arrive_expect_tx(&full[s], bytes);  // publishes slot + run info (release)
-                int sh;
-                stage_range(pr, lo, hi, st, &full[s], sh);
-                if (qr) stage_range(qr, lo, hi, st + kHalfStride, &full[s], sh);
-                ++n;
+            ++as.issued;
+        }
+        cp_async_wait_pending(as.issued - as.consumed - 1);  // chunk k has landed (this thread's copies)
+        const int c = cur.c0 + k;
+        const uint4* st = ring + (size_t)(as.consumed % kAStages) * CV;
+        ++as.consumed;
+        uint4 w[kAVec];
+        // CTA-uniform: only a row's first chunk (misaligned start) and its last
+        // (partial / past-the-end vectors) need masking.
+        const bool edge = (c == 0 && shift) || (c + 1) * CV > nvec_row - (tail ? 1 : 0);
+        if (!edge) {
+#pragma unroll
+            for (int j = 0; j < kAVec; ++j) w[j] = st[j * kCtaThreads + tid];
+        } else {
+#pragma unroll
+            for (int j = 0; j < kAVec; ++j) {
+                const int v = c * CV + tid + kCtaThreads * j;
+                w[j] = v < nvec_row ? st[j * kCtaThreads + tid] : pad_vec<T>();
+                if (v == 0 && shift) mask_vec<T>(w[j], shift, VEC);        // the row's first vector
+                if (v == nvec_row - 1 && tail) mask_vec<T>(w[j], 0, tail);  // and its last
+            }
+        }
+        if constexpr (sizeof(T) == 8) {
+            double cm = -DBL_MAX;
+#pragma unroll
+            for (int j = 0; j < kAVec; ++j) {
+                double x[2];
+                unpack(w[j], x);
+                cm = fmax(cm, fmax(x[0], x[1]));
+                mn = fmin(mn, fmin(x[0], x[1]));
+            }
+            if (cm > m) {
+                if (s != 0.0) s *= exp(m - cm);
+                m = cm;
+            }
+            if (m != -DBL_MAX) {
+#pragma unroll
+                for (int j = 0; j < kAVec; ++j) {
+                    double x[2];
+                    unpack(w[j], x);
+                    s += exp(x[0] - m) + exp(x[1] - m);
+                }
             }
         } else {
-            unsigned s;
-            stage(s);
-            Slot sl;
-            sl.type = it.type;
-            sl.ctx = -1;
-            sl.pos = 0;
-            sl.b = it.b;
-            sl.mode = it.mode;
-            sl.row = it.row;
-            sl.Mp = it.Mp;
-            sl.Sp = it.Sp;
-            sl.Mq = it.Mq;
-            sl.Sq = it.Sq;
-            slots[s] = sl;
-            mbar_arrive(&full[s]);
-            ++n;
-            if (it.type == IT_STOP) break;
+            float cm = -FLT_MAX;
+#pragma unroll
+            for (int j = 0; j < kAVec; ++j) AStat<T>::minmax(w[j], cm, mn);
+            // The thread's max grew: rescale its running sum (fp64).  A warp vote
+            // keeps this a real (rarely taken) branch instead of predicated code.
+            if (__any_sync(kFull, cm > m)) {
+                if (cm > m) {
+                    if (s != 0.0) s *= exp((double)m - (double)cm);
+                    m = cm;
+                }
+            }
+            if (m != -FLT_MAX) {  // a thread that has seen pads only contributes nothing
+                const float2 negM = make_float2(-m, -m);
+                float2 s0 = make_float2(0.f, 0.f), s1 = make_float2(0.f, 0.f);
+#pragma unroll
+                for (int j = 0; j < kAVec; ++j) {
+                    if (j & 1) AStat<T>::expsum(w[j], negM, s1);
+                    else AStat<T>::expsum(w[j], negM, s0);
+                }
+                s += ((double)s0.x + (double)s0.y) + ((double)s1.x + (double)s1.y);
+            }
         }
+    }
+    as.next_pre = nxt_issued;
+    // -inf logit (require_finite, dist.cpp:27-36); NaN / +inf surface in the sum
+    if (__any_sync(kFull, isinf(mn)) && lane == 0) flag(P, SSV_STATUS_NONFINITE);
+    // Warp fold (fixed order, fp64) -> one partial per warp; no CTA barrier, so
+    // the warps of a CTA drift freely between runs.
+    const double md = (double)m;
+    double M = warp_max(md);
+    const double S = warp_sum(s != 0.0 ? s * exp(md - M) : s);  // NaN propagates
+    if (lane == 0) {
+        if (isnan(S) || M == CUDART_INF) flag(P, SSV_STATUS_NONFINITE);
+        if (S == 0.0) M = -CUDART_INF;  // a warp that saw pads only
+        P.part[(((size_t)b * P.NR + r) * P.K + q) * kWarps + warp] = make_double2(M, S);
+        red_release_add(&P.cnt1[b], 1u);  // release: the partial is visible first
     }
 }
 
@@ -395,64 +399,88 @@ __device__ void producer(const StepParams& P, uint8_t* stages, uint64_t* full, u
 // Decisions.  Exact: row statistics from the A-item partials (fixed order,
 // fp64), tau at every drafted position from the gathered logits (fp64;
 // activation.cpp:20-27 + verify_reference.cpp:87-92), first rejection
-// (verify_reference.cpp:93-96, inclusive u <= tau).
+// (verify_reference.cpp:93-96, inclusive u <= tau).  Runs on the CTA that
+// completed the row's last A-item; publishes Decision + release flag.
 template <typename T>
-__device__ void decide_exact(const StepParams& P, int b, double* s_red, int* s_ired, double2* s_rs) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+__device__ void item_D(const StepParams& P, int b, Shared& sh) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int G = P.G;
-    // gathers and uniforms first: their latency overlaps the row statistics
-    const int c = threadIdx.x;
+    // The gathers and uniforms do not depend on the row statistics: issue
+    // them before waiting so their latency overlaps the A-items' tail.
     double zp = 0.0, zq = 0.0, u = 0.0;
-    if (c < G) {
-        int x = P.ids[(size_t)b * G + c];
+    if (tid < G) {
+        int x = P.ids[(size_t)b * G + tid];
         if (x < 0 || x >= P.V) {
             flag(P, SSV_STATUS_TOKEN_RANGE);
             x = x < 0 ? 0 : P.V - 1;
         }
-        zp = load_exact(p_row<T>(P, b, c) + x);
-        zq = load_exact(q_row<T>(P, b, c) + x);
+        zp = load_exact(p_row<T>(P, b, tid) + x);
+        zq = load_exact(q_row<T>(P, b, tid) + x);
     }
-    if (c <= G) u = P.u[(size_t)b * (G + 1) + c];
-    if (P.check_uniforms && c <= G && (!(u >= 0.0) || !(u < 1.0))) flag(P, SSV_STATUS_UNIFORM_RANGE);
-    for (int r = warp; r < P.NR; r += kConsWarps) {
-        const double2* part = P.part + ((size_t)b * P.NR + r) * P.RPR;
+    if (tid <= G) u = P.u[(size_t)b * (G + 1) + tid];
+    if (tid == 0) wait_geq(&P.cnt1[b], (unsigned)P.nA * kWarps);
+    __syncthreads();
+    const int KP = P.K * kWarps;  // partials per statistics row
+    for (int r = warp; r < P.NR; r += kWarps) {
+        const double2* part = P.part + ((size_t)b * P.NR + r) * KP;
         double2 pk[4];
         double m = -CUDART_INF;
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
             const int k = lane + 32 * i;
-            pk[i] = k < P.RPR ? __ldcg(&part[k]) : make_double2(-CUDART_INF, 0.0);
+            pk[i] = k < KP ? __ldcg(&part[k]) : make_double2(-CUDART_INF, 0.0);
             m = fmax(m, pk[i].x);
         }
-        for (int k = lane + 128; k < P.RPR; k += 32) m = fmax(m, __ldcg(&part[k].x));
+        for (int k = lane + 128; k < KP; k += 32) m = fmax(m, __ldcg(&part[k].x));
         m = warp_max(m);
         double sm = 0.0;
 #pragma unroll
         for (int i = 0; i < 4; ++i)
-            if (pk[i].y > 0.0) sm += pk[i].y * exp(pk[i].x - m);
-        for (int k = lane + 128; k < P.RPR; k += 32) {
+            if (pk[i].y != 0.0) sm += pk[i].y * exp(pk[i].x - m);  // NaN propagates
+        for (int k = lane + 128; k < KP; k += 32) {
             const double2 v = __ldcg(&part[k]);
-            if (v.y > 0.0) sm += v.y * exp(v.x - m);
+            if (v.y != 0.0) sm += v.y * exp(v.x - m);
         }
         sm = warp_sum(sm);
         if (lane == 0) {
+            if (!isfinite(m) || !isfinite(sm)) flag(P, SSV_STATUS_NONFINITE);  // NaN / +inf logit
             P.rowstat[(size_t)b * P.NR + r] = make_double2(m, sm);
-            if (r < kMaxRowsSmem) s_rs[r] = make_double2(m, sm);
+            if (r < kMaxRowsSmem) sh.rs[r] = make_double2(m, sm);
         }
     }
-    cbar<kCons>();
-    auto rs = [&](int r) -> double2 { return r < kMaxRowsSmem ? s_rs[r] : P.rowstat[(size_t)b * P.NR + r]; };
-    int rej = 0x7fffffff;
-    if (c < G) {
+    __syncthreads();
+    auto rs = [&](int r) -> double2 { return r < kMaxRowsSmem ? sh.rs[r] : __ldcg(&P.rowstat[(size_t)b * P.NR + r]); };
+    auto tau_at = [&](int c, double zpc, double zqc) -> double {
         const double2 sp = rs(c), sq = rs(G + c);
-        const double p = exp(zp - sp.x) / sp.y;   // activation.cpp:20-27, dist.cpp:46-50
-        const double q = exp(zq - sq.x) / sq.y;
-        const double tau = ratio_clamped(p, q);
-        P.tau[(size_t)b * G + c] = tau;
-        if (!(u <= tau)) rej = c;                // verify_reference.cpp:93-96 (inclusive)
+        const double p = exp(zpc - sp.x) / sp.y;  // activation.cpp:20-27, dist.cpp:46-50
+        const double q = exp(zqc - sq.x) / sq.y;
+        return ratio_clamped(p, q);
+    };
+    int rej = 0x7fffffff;
+    if (tid < G) {
+        const double tau = tau_at(tid, zp, zq);
+        P.tau[(size_t)b * G + tid] = tau;
+        if (!(u <= tau)) rej = tid;  // verify_reference.cpp:93-96 (inclusive)
     }
-    const int a = min(creduce(rej, s_ired, OpMin()), G);
-    if (threadIdx.x == 0) {
+    for (int c = tid + kCtaThreads; c < G; c += kCtaThreads) {  // gamma > 256
+        int x = P.ids[(size_t)b * G + c];
+        if (x < 0 || x >= P.V) {
+            flag(P, SSV_STATUS_TOKEN_RANGE);
+            x = x < 0 ? 0 : P.V - 1;
+        }
+        const double tau = tau_at(c, load_exact(p_row<T>(P, b, c) + x), load_exact(q_row<T>(P, b, c) + x));
+        P.tau[(size_t)b * G + c] = tau;
+        if (!(P.u[(size_t)b * (G + 1) + c] <= tau)) rej = min(rej, c);
+    }
+    if (P.check_uniforms) {
+        if (tid <= G && (!(u >= 0.0) || !(u < 1.0))) flag(P, SSV_STATUS_UNIFORM_RANGE);
+        for (int c = tid + kCtaThreads; c <= G; c += kCtaThreads) {
+            const double uc = P.u[(size_t)b * (G + 1) + c];
+            if (!(uc >= 0.0) || !(uc < 1.0)) flag(P, SSV_STATUS_UNIFORM_RANGE);
+        }
+    }
+    const int a = min(block_reduce(rej, sh.ired, OpMin()), G);
+    if (tid == 0) {
         P.acc[b] = a;
         Decision d{};
         if (a < G) {
@@ -473,17 +501,17 @@ __device__ void decide_exact(const StepParams& P, int b, double* s_red, int* s_i
             P.rden[b] = 0.0;
         }
         P.dec[b] = d;
-        P.cnt1[b] = 0;  // every A-item of b has been counted (the producer waited for it)
-        __threadfence();
-        st_release(&P.flag[b], P.epoch);
+        P.cnt1[b] = 0;  // every A-item of b has been counted
+        st_release(&P.flag[b], 1u);
     }
 }
 
-// Sigmoid / probability decision from the gathered logits only (one warp).
-// verify_sigmoid.cpp:50-58 -> verify_reference.cpp:87-96; the sigmoid is
-// evaluated in fp64 exactly as dist.cpp:60-62 does.
+// Sigmoid / probability decision from the gathered values only (warp 0 of a
+// B-item).  verify_sigmoid.cpp:50-58 -> verify_reference.cpp:87-96; the
+// sigmoid is evaluated in fp64 exactly as dist.cpp:60-62 does.  Only the
+// row's first B-item writes the outputs; the others recompute identically.
 template <typename T, int ACT>
-__device__ void decide_gather(const StepParams& P, int b) {
+__device__ void decide_gather(const StepParams& P, int b, bool write, Decision& out) {
     const int lane = threadIdx.x & 31;
     const int G = P.G;
     int accepted = G;
@@ -493,7 +521,7 @@ __device__ void decide_gather(const StepParams& P, int b) {
         if (c < G) {
             int x = P.ids[(size_t)b * G + c];
             if (x < 0 || x >= P.V) {
-                flag(P, SSV_STATUS_TOKEN_RANGE);
+                if (write) flag(P, SSV_STATUS_TOKEN_RANGE);
                 x = x < 0 ? 0 : P.V - 1;
             }
             const double zp = load_exact(p_row<T>(P, b, c) + x);
@@ -505,19 +533,38 @@ __device__ void decide_gather(const StepParams& P, int b) {
             } else {
                 p = zp;
                 q = zq;
-                if (p < 0.0 || q < 0.0) flag(P, SSV_STATUS_NEGATIVE);
+                if (write && (p < 0.0 || q < 0.0)) flag(P, SSV_STATUS_NEGATIVE);
             }
             const double tau = ratio_clamped(p, q);
-            P.tau[(size_t)b * G + c] = tau;
+            if (write) P.tau[(size_t)b * G + c] = tau;
             rej = !(P.u[(size_t)b * (G + 1) + c] <= tau);
         }
         const unsigned m = __ballot_sync(kFull, rej);
         if (m) {
             accepted = c0 + __ffs(m) - 1;
+            if (write) {  // tau past the first rejection is still reported (step.hpp:39-41)
+                for (int c2 = c0 + 32 + lane; c2 < G; c2 += 32) {
+                    int x = P.ids[(size_t)b * G + c2];
+                    if (x < 0 || x >= P.V) {
+                        flag(P, SSV_STATUS_TOKEN_RANGE);
+                        x = x < 0 ? 0 : P.V - 1;
+                    }
+                    const double zp = load_exact(p_row<T>(P, b, c2) + x);
+                    const double zq = load_exact(q_row<T>(P, b, c2) + x);
+                    double p = zp, q = zq;
+                    if (ACT == ACT_SIGMOID) {
+                        p = sigmoid_scaled_d(zp, P.alpha, P.width);
+                        q = sigmoid_scaled_d(zq, P.alpha, P.width);
+                    } else if (p < 0.0 || q < 0.0) {
+                        flag(P, SSV_STATUS_NEGATIVE);
+                    }
+                    P.tau[(size_t)b * G + c2] = ratio_clamped(p, q);
+                }
+            }
             break;
         }
     }
-    if (P.check_uniforms) {
+    if (write && P.check_uniforms) {
         for (int c = lane; c <= G; c += 32) {
             const double u = P.u[(size_t)b * (G + 1) + c];
             if (!(u >= 0.0) || !(u < 1.0)) flag(P, SSV_STATUS_UNIFORM_RANGE);
@@ -526,7 +573,6 @@ __device__ void decide_gather(const StepParams& P, int b) {
     if (lane == 0) {
         Decision d{};
         d.Sp = d.Sq = 1.0;
-        P.acc[b] = accepted;
         if (accepted < G) {
             d.mode = MODE_REJECT;
             d.row = accepted;
@@ -535,13 +581,16 @@ __device__ void decide_gather(const StepParams& P, int b) {
             d.row = G;
         } else {
             d.mode = MODE_NONE;
-            P.fin[b] = -1;
-            P.rsu[b] = 0;
-            P.rden[b] = 0.0;
         }
-        P.dec[b] = d;
-        __threadfence();
-        st_release(&P.flag[b], P.epoch);
+        if (write) {
+            P.acc[b] = accepted;
+            if (d.mode == MODE_NONE) {
+                P.fin[b] = -1;
+                P.rsu[b] = 0;
+                P.rden[b] = 0.0;
+            }
+        }
+        out = d;
     }
 }
 
@@ -576,39 +625,124 @@ __device__ __forceinline__ double exact_value(const StepParams& P, const RowCtx&
 }
 
 // ---------------------------------------------------------------------------
-// Inverse CDF of batch row b (consumer group): granule partials -> SMEM ->
-// fp64 granule prefix (contiguous ownership, one scan) -> exact fp64 scan
-// inside the selected granule (dist.cpp:122-137, incl. both fallbacks).
+// B-item granule: warp w reduces granule j*8 + w of the needed row(s) (coalesced
+// element loads; rows of odd length have arbitrary alignment) to
+//   reject:  (sum max(0, p - q), sum p)          -- residual / fallback masses
+//   bonus:   (max, sum e^(x - max)) [softmax]  or  (0, sum value)
 template <typename T, int ACT>
-__device__ void locate(const StepParams& P, const Slot& it, double2* gcache, double* s_red, int* s_ired) {
-    const int b = it.b, NG = P.NG, GW = P.GW;
+__device__ void granule(const StepParams& P, int b, int g, const Decision& d, double2* gp) {
+    using A = typename Elem<T>::acc;
+    constexpr int EPL = kGW / 32;  // elements per lane per row (16)
+    const int lane = threadIdx.x & 31;
+    const int lo = g * kGW, n = min(kGW, P.V - lo);
+    const bool reject = d.mode == MODE_REJECT;
+    const T* pr = p_row<T>(P, b, d.row) + lo;
+    const T* qr = reject ? q_row<T>(P, b, d.row) + lo : pr;
+    const A alpha = (A)P.alpha, invw = (A)(1.0 / P.width);
+    A xs[EPL], xq[EPL];
+#pragma unroll
+    for (int t = 0; t < EPL; ++t) {
+        const int e = t * 32 + lane;
+        xs[t] = e < n ? load_elem(pr + e) : (A)0;
+        xq[t] = (reject && e < n) ? load_elem(qr + e) : (A)0;
+    }
+    double2 out;
+    if (!reject) {
+        if (ACT == ACT_SOFTMAX) {
+            A mx = -INFINITY, mn = INFINITY;
+#pragma unroll
+            for (int t = 0; t < EPL; ++t)
+                if (t * 32 + lane < n) {
+                    mx = fmax(mx, xs[t]);
+                    mn = fmin(mn, xs[t]);
+                }
+            mx = warp_max(mx);
+            mn = warp_min(mn);
+            A sm = 0;
+#pragma unroll
+            for (int t = 0; t < EPL; ++t)
+                if (t * 32 + lane < n) sm += exp_rel(xs[t], mx);
+            const double S = warp_sum((double)sm);
+            if (lane == 0 && (!isfinite((double)mx) || isnan(S) || !isfinite((double)mn)))
+                flag(P, SSV_STATUS_NONFINITE);
+            out = make_double2((double)mx, S);
+        } else {
+            A sm = 0;
+#pragma unroll
+            for (int t = 0; t < EPL; ++t) {
+                if (t * 32 + lane < n) {
+                    if (ACT == ACT_SIGMOID) sm += (A)1 / ((A)1 + exp_neg((xs[t] - alpha) * invw));
+                    else sm += xs[t];
+                }
+            }
+            out = make_double2(0.0, warp_sum((double)sm));
+        }
+    } else {
+        const A Mp = (A)d.Mp, Mq = (A)d.Mq, iSp = (A)(1.0 / d.Sp), iSq = (A)(1.0 / d.Sq);
+        A ta = 0, tp = 0;
+#pragma unroll
+        for (int t = 0; t < EPL; ++t) {
+            if (t * 32 + lane < n) {
+                const A xp = xs[t], xqq = xq[t];
+                A a, vp;
+                if (ACT == ACT_SOFTMAX) {
+                    vp = exp_rel(xp, Mp) * iSp;
+                    const A vq = exp_rel(xqq, Mq) * iSq;
+                    a = vp - vq > (A)0 ? vp - vq : (A)0;
+                } else if (ACT == ACT_SIGMOID) {
+                    // sigma(tp) - sigma(tq) = sigma(tp) sigma(-tq) (1 - e^-(tp-tq)): no cancellation.
+                    const A tp_ = (xp - alpha) * invw, tq_ = (xqq - alpha) * invw;
+                    const A dd = (xp - xqq) * invw;
+                    vp = (A)1 / ((A)1 + exp_neg(tp_));
+                    const A sqn = (A)1 / ((A)1 + exp_neg(-tq_));
+                    a = dd > (A)0 ? vp * sqn * (-expm1_acc(-dd)) : (A)0;
+                } else {
+                    vp = xp;
+                    a = xp - xqq > (A)0 ? xp - xqq : (A)0;
+                }
+                ta += a;
+                tp += vp;
+            }
+        }
+        out = make_double2(warp_sum((double)ta), warp_sum((double)tp));
+    }
+    if (lane == 0) *gp = out;
+}
+
+// ---------------------------------------------------------------------------
+// Inverse CDF of batch row b (whole CTA): granule partials -> SMEM -> fp64
+// granule prefix (contiguous ownership, one scan) -> exact fp64 scan inside
+// the selected granule (dist.cpp:122-137, incl. both fallbacks).
+template <typename T, int ACT>
+__device__ void locate(const StepParams& P, int b, const Decision& d, Shared& sh, double2* gcache) {
+    const int NG = P.NG, GW = kGW;
     const double2* gp = P.gpart + (size_t)b * NG;
-    const T* pr = p_row<T>(P, b, it.row);
-    const T* qr = it.mode == MODE_REJECT ? q_row<T>(P, b, it.row) : nullptr;
+    const T* pr = p_row<T>(P, b, d.row);
+    const T* qr = d.mode == MODE_REJECT ? q_row<T>(P, b, d.row) : nullptr;
     const double u = __ldcg(&P.u[(size_t)b * (P.G + 1) + P.G]);  // u_final, verify_reference.cpp:98
     const int ncache = min(NG, kLocCap);
-    for (int g = threadIdx.x; g < ncache; g += kCons) gcache[g] = __ldcg(&gp[g]);
-    cbar<kCons>();
+    for (int g = threadIdx.x; g < ncache; g += kCtaThreads) gcache[g] = __ldcg(&gp[g]);
+    __syncthreads();
     auto raw = [&](int g) -> double2 { return g < kLocCap ? gcache[g] : __ldcg(&gp[g]); };
 
     RowCtx R;
-    R.mode = it.mode;
-    R.Mp = it.Mp;
-    R.Sp = it.Sp;
-    R.Mq = it.Mq;
-    R.Sq = it.Sq;
+    R.mode = d.mode;
+    R.Mp = d.Mp;
+    R.Sp = d.Sp;
+    R.Mq = d.Mq;
+    R.Sq = d.Sq;
     R.useA = false;
     R.denom = 1.0;
     double gM = 0.0, gS = 1.0;
-    if (it.mode == MODE_REJECT) {
+    if (d.mode == MODE_REJECT) {
         double sa = 0.0, sp = 0.0;
-        for (int g = threadIdx.x; g < NG; g += kCons) {
+        for (int g = threadIdx.x; g < NG; g += kCtaThreads) {
             const double2 v = raw(g);
             sa += v.x;
             sp += v.y;
         }
-        sa = creduce(sa, s_red, OpSum());
-        sp = creduce(sp, s_red, OpSum());
+        sa = block_reduce(sa, sh.dred, OpSum());
+        sp = block_reduce(sp, sh.dred, OpSum());
         R.useA = sa > kZeroEps;  // verify_reference.cpp:57-62
         R.denom = R.useA ? sa : sp;
         if (threadIdx.x == 0) {
@@ -618,21 +752,21 @@ __device__ void locate(const StepParams& P, const Slot& it, double2* gcache, dou
     } else {
         if (ACT == ACT_SOFTMAX) {  // the bonus row's statistics from its granules
             double m = -CUDART_INF;
-            for (int g = threadIdx.x; g < NG; g += kCons) m = fmax(m, raw(g).x);
-            gM = creduce(m, s_red, OpMax());
+            for (int g = threadIdx.x; g < NG; g += kCtaThreads) m = fmax(m, raw(g).x);
+            gM = block_reduce(m, sh.dred, OpMax());
             double sm = 0.0;
-            for (int g = threadIdx.x; g < NG; g += kCons) {
+            for (int g = threadIdx.x; g < NG; g += kCtaThreads) {
                 const double2 v = raw(g);
                 if (v.y > 0.0) sm += v.y * exp(v.x - gM);
             }
-            gS = creduce(sm, s_red, OpSum());
+            gS = block_reduce(sm, sh.dred, OpSum());
             R.Mp = gM;
             R.Sp = gS;
             R.denom = 1.0;  // sample_row's sequential_sum of a softmax row (1 within rounding)
         } else {
             double sm = 0.0;
-            for (int g = threadIdx.x; g < NG; g += kCons) sm += raw(g).y;
-            R.denom = creduce(sm, s_red, OpSum());
+            for (int g = threadIdx.x; g < NG; g += kCtaThreads) sm += raw(g).y;
+            R.denom = block_reduce(sm, sh.dred, OpSum());
         }
         if (threadIdx.x == 0) {
             if (P.rsu) P.rsu[b] = 0;
@@ -647,12 +781,12 @@ __device__ void locate(const StepParams& P, const Slot& it, double2* gcache, dou
     };
 
     // Level 1: contiguous granule ownership, one block scan.
-    const int gpt = (NG + kCons - 1) / kCons;
-    const int ga = min(NG, threadIdx.x * gpt), gb = min(NG, ga + gpt);
+    const int gpt = (NG + kCtaThreads - 1) / kCtaThreads;
+    const int ga = min(NG, (int)threadIdx.x * gpt), gb = min(NG, ga + gpt);
     double tsum = 0.0;
     for (int g = ga; g < gb; ++g) tsum += gmass(g);
     double total;
-    double run = cscan_incl(tsum, s_red, total) - tsum;
+    double run = block_scan_incl(tsum, sh.dred, total) - tsum;
     int hit = 0x7fffffff;
     double hit_carry = 0.0;
     for (int g = ga; g < gb; ++g) {
@@ -664,36 +798,38 @@ __device__ void locate(const StepParams& P, const Slot& it, double2* gcache, dou
         }
         run += w;
     }
-    int gstar = creduce(hit, s_ired, OpMin());
+    int gstar = block_reduce(hit, sh.ired, OpMin());
     double carry = 0.0;
     if (gstar != 0x7fffffff) {
-        if (hit == gstar) s_red[0] = hit_carry;  // creduce's barriers ordered every earlier s_red read
-        cbar<kCons>();
-        carry = s_red[0];
+        if (hit == gstar) sh.dred[0] = hit_carry;  // block_reduce's barriers ordered every earlier dred read
+        __syncthreads();
+        carry = sh.dred[0];
     } else {
         gstar = -1;
     }
 
     // Level 2: exact element scan, continuing into later granules on rounding.
     int token = -1;
-    const int E = (GW + kCons - 1) / kCons;  // elements per thread (1 or 2)
+    constexpr int E = (kGW + kCtaThreads - 1) / kCtaThreads;  // elements per thread (2)
+    static_assert(E == 2, "level-2 scan assumes two elements per thread");
     while (gstar >= 0 && gstar < NG) {
         const int lo = gstar * GW;
         const int hi = min(lo + GW, P.V);
         const int base = lo + threadIdx.x * E;
         double v0 = 0.0, v1 = 0.0;
         if (base < hi) v0 = exact_value<T, ACT>(P, R, pr, qr, base) / R.denom;
-        if (E > 1 && base + 1 < hi) v1 = exact_value<T, ACT>(P, R, pr, qr, base + 1) / R.denom;
+        if (base + 1 < hi) v1 = exact_value<T, ACT>(P, R, pr, qr, base + 1) / R.denom;
         const double ts = v0 + v1;
         double tot;
-        const double incl = cscan_incl(ts, s_red, tot);
+        __syncthreads();  // sh.dred[0] (carry) has been read by every thread
+        const double incl = block_scan_incl(ts, sh.dred, tot);
         double cum = carry + (incl - ts);
         int h = 0x7fffffff;
         cum += v0;
         if (base < hi && u < cum) h = base;
         cum += v1;
-        if (h == 0x7fffffff && E > 1 && base + 1 < hi && u < cum) h = base + 1;
-        const int first = creduce(h, s_ired, OpMin());
+        if (h == 0x7fffffff && base + 1 < hi && u < cum) h = base + 1;
+        const int first = block_reduce(h, sh.ired, OpMin());
         if (first != 0x7fffffff) {
             token = first;
             break;
@@ -704,322 +840,147 @@ __device__ void locate(const StepParams& P, const Slot& it, double2* gcache, dou
     if (token < 0) {
         // dist.cpp:135-136: last index with positive mass, else 0.
         int glast = -1;
-        for (int g = threadIdx.x; g < NG; g += kCons)
+        for (int g = threadIdx.x; g < NG; g += kCtaThreads)
             if (gmass(g) > 0.0) glast = max(glast, g);
-        glast = creduce(glast, s_ired, OpMax());
+        glast = block_reduce(glast, sh.ired, OpMax());
         token = 0;
         if (glast >= 0) {
             int last = -1;
-            for (int i = glast * GW + threadIdx.x; i < min((glast + 1) * GW, P.V); i += kCons)
+            for (int i = glast * GW + threadIdx.x; i < min((glast + 1) * GW, P.V); i += kCtaThreads)
                 if (exact_value<T, ACT>(P, R, pr, qr, i) > 0.0) last = max(last, i);
-            last = creduce(last, s_ired, OpMax());
+            last = block_reduce(last, sh.ired, OpMax());
             if (last >= 0) token = last;
         }
     }
-    if (threadIdx.x == 0) {
-        P.fin[b] = token;
-        P.cnt2[b] = 0;  // every B-item of b has been counted (the producer waited for it)
-    }
+    if (threadIdx.x == 0) P.fin[b] = token;
 }
 
-// ---------------------------------------------------------------------------
-__device__ __forceinline__ void red_release_add(unsigned* p, unsigned v) {
-    asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-
-// Lane 0 of each warp counts the warp out of run `ri`; true in exactly one
-// warp per run (the last), after every other warp's writes to `ri`.
-__device__ __forceinline__ bool run_last_warp(RunInfo& ri) {
-    unsigned old = 0;
-    if ((threadIdx.x & 31) == 0) {
-        __threadfence_block();
-        old = atomicAdd(&ri.cnt, 1u);
-        __threadfence_block();
-    }
-    old = __shfl_sync(kFull, old, 0);
-    return old == kConsWarps - 1;
-}
-
-// Per-lane online softmax state of the A-run in flight.
-template <typename A>
-struct LaneRun {
-    A m, mn;
-    double s;
-};
-
-// A-chunk: the warp copies its 1/8 of the staged chunk into registers, frees
-// the stage, then folds it into the lane's running (max, sum e^(x - max), min)
-// -- fp32 ex2 within the chunk, fp64 across chunks, an fp64 exp only when the
-// lane's max grows.  No cross-lane work until the run's last chunk.
-template <typename T>
-__device__ __forceinline__ void chunk_A(const StepParams& P, const uint8_t* st, int shift, int n,
-                                        LaneRun<typename Elem<T>::acc>& L, uint64_t* empty_s) {
-    using A = typename Elem<T>::acc;
-    constexpr int VEC = Elem<T>::VEC;
-    constexpr int WPW = kStageBytes / 16 / kConsWarps;  // 16-byte words per warp (128)
-    constexpr int M = WPW / 32;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int end = shift + n;                          // valid element range in the stage
-    const int nwords = (end * (int)sizeof(T) + 15) / 16;  // <= 1025
-    const int w0 = warp * WPW;
-    const int w1 = min(nwords, w0 + WPW);
-    uint4 w[M];
-    uint4 wx;  // the 1025th word of a misaligned chunk (warp 7, lane 0)
-    const bool has_x = warp == kConsWarps - 1 && lane == 0 && nwords > kConsWarps * WPW;
-#pragma unroll
-    for (int m = 0; m < M; ++m) {
-        const int wi = w0 + lane + 32 * m;
-        if (wi < w1) w[m] = *reinterpret_cast<const uint4*>(st + (size_t)wi * 16);
-    }
-    if (has_x) wx = *reinterpret_cast<const uint4*>(st + (size_t)(kConsWarps * WPW) * 16);
-    __syncwarp();
-    if (lane == 0) mbar_arrive(empty_s);  // the stage is free for the producer
-    A cm = -INFINITY, cn = INFINITY;
-    auto scan_word = [&](const uint4& v, int wi, auto&& f) {
-        A x[VEC];
-        unpack(v, x);
-        if (wi * VEC >= shift && (wi + 1) * VEC <= end) {
-#pragma unroll
-            for (int e = 0; e < VEC; ++e) f(x[e]);
-        } else {
-#pragma unroll
-            for (int e = 0; e < VEC; ++e) {
-                const int idx = wi * VEC + e;
-                if (idx >= shift && idx < end) f(x[e]);
-            }
-        }
-    };
-    auto mm = [&](A x) {
-        cm = fmax(cm, x);
-        cn = fmin(cn, x);
-    };
-#pragma unroll
-    for (int m = 0; m < M; ++m) {
-        const int wi = w0 + lane + 32 * m;
-        if (wi < w1) scan_word(w[m], wi, mm);
-    }
-    if (has_x) scan_word(wx, kConsWarps * WPW, mm);
-    if (cm > L.m) {  // the lane's max grew: rescale its running sum (fp64)
-        if (L.s > 0.0) L.s *= exp((double)L.m - (double)cm);
-        L.m = cm;
-    }
-    L.mn = fmin(L.mn, cn);
-    if (L.m > -INFINITY) {
-        A t = 0;
-        const A mref = L.m;
-        auto ex = [&](A x) { t += exp_rel(x, mref); };
-#pragma unroll
-        for (int m = 0; m < M; ++m) {
-            const int wi = w0 + lane + 32 * m;
-            if (wi < w1) scan_word(w[m], wi, ex);
-        }
-        if (has_x) scan_word(wx, kConsWarps * WPW, ex);
-        L.s += (double)t;
-    }
-}
-
-// End of an A-run: warp partial, and the run's last warp folds the 8 warp
-// partials (fixed order) and publishes ONE (max, sum) per run.
-template <typename A>
-__device__ void finish_A(const StepParams& P, RunInfo& ri, LaneRun<A>& L) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    if (isnan(L.s)) flag(P, SSV_STATUS_NONFINITE);  // NaN logit (require_finite, dist.cpp:27-36)
-    const double lm = (double)L.m;
-    const double M = warp_max(lm);
-    const double S = warp_sum(L.s > 0.0 ? L.s * exp(lm - M) : 0.0);
-    const double MN = warp_min((double)L.mn);
-    if (lane == 0) {
-        if (isnan(S)) flag(P, SSV_STATUS_NONFINITE);  // NaN logit (require_finite, dist.cpp:27-36)
-        ri.wpart[warp] = make_double2(M, S);
-        ri.wmin[warp] = MN;
-    }
-    if (!run_last_warp(ri)) return;
-    const double2 wp = lane < kConsWarps ? ri.wpart[lane] : make_double2(-CUDART_INF, 0.0);
-    const double MX = warp_max(wp.x);
-    const double SX = warp_sum(wp.y > 0.0 ? wp.y * exp(wp.x - MX) : 0.0);
-    const double MNX = warp_min(lane < kConsWarps ? ri.wmin[lane] : CUDART_INF);
-    if (lane == 0) {
-        ri.cnt = 0;
-        P.part[((size_t)ri.b * P.NR + ri.r) * P.RPR + ri.q] = make_double2(MX, SX);
-        if (!isfinite(MX) || isnan(SX) || !isfinite(MNX)) flag(P, SSV_STATUS_NONFINITE);
-        __threadfence();
-        red_release_add(&P.cnt1[ri.b], 1u);
-    }
-}
-
-// B-chunk: each warp copies its granule (both rows for a rejection) into
-// registers, frees the stage, and reduces the granule; the run's last warp
-// publishes the run's granule partials.
+// The decision a B- or L-item works from.  Exact: wait for the D-item's
+// release flag.  Sampling: the bonus row is row 0.  Sigmoid / probabilities:
+// recompute it from the gathered values (warp 0; the L-item writes outputs).
 template <typename T, int ACT>
-__device__ void chunk_B(const StepParams& P, RunInfo& ri, const uint8_t* st, int pos, int n, uint64_t* empty_s) {
-    using A = typename Elem<T>::acc;
-    constexpr int EPL = kStageBytes / 2 / (int)sizeof(T) / kCons;  // elements per lane per granule
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int e0 = warp * P.GW;
-    const bool reject = ri.mode == MODE_REJECT;
-    const A alpha = (A)P.alpha, invw = (A)(1.0 / P.width);
-    A xs[EPL], xq[EPL];
-#pragma unroll
-    for (int t = 0; t < EPL; ++t) {
-        const int e = e0 + t * 32 + lane;
-        xs[t] = e < n ? lds_elem<T>(st, ri.shift_p + e) : (A)0;
-        xq[t] = (reject && e < n) ? lds_elem<T>(st + kHalfStride, ri.shift_q + e) : (A)0;
-    }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(empty_s);
-    double2 out = make_double2(0.0, 0.0);
-    if (e0 < n) {
-        if (!reject) {
-            if (ACT == ACT_SOFTMAX) {
-                A mx = -INFINITY, mn = INFINITY;
-#pragma unroll
-                for (int t = 0; t < EPL; ++t)
-                    if (e0 + t * 32 + lane < n) {
-                        mx = fmax(mx, xs[t]);
-                        mn = fmin(mn, xs[t]);
-                    }
-                mx = warp_max(mx);
-                mn = warp_min(mn);
-                A sm = 0;
-#pragma unroll
-                for (int t = 0; t < EPL; ++t)
-                    if (e0 + t * 32 + lane < n) sm += exp_rel(xs[t], mx);
-                const double S = warp_sum((double)sm);
-                if (lane == 0 && (!isfinite((double)mx) || isnan(S) || !isfinite((double)mn)))
-                    flag(P, SSV_STATUS_NONFINITE);
-                out = make_double2((double)mx, S);
-            } else {
-                A sm = 0;
-#pragma unroll
-                for (int t = 0; t < EPL; ++t) {
-                    if (e0 + t * 32 + lane < n) {
-                        if (ACT == ACT_SIGMOID) sm += (A)1 / ((A)1 + exp_neg((xs[t] - alpha) * invw));
-                        else sm += xs[t];
-                    }
-                }
-                out = make_double2(0.0, warp_sum((double)sm));
-            }
-        } else {
-            const A Mp = (A)ri.Mp, Mq = (A)ri.Mq, iSp = (A)(1.0 / ri.Sp), iSq = (A)(1.0 / ri.Sq);
-            A ta = 0, tp = 0;
-#pragma unroll
-            for (int t = 0; t < EPL; ++t) {
-                if (e0 + t * 32 + lane < n) {
-                    const A xp = xs[t], xqq = xq[t];
-                    A a, vp;
-                    if (ACT == ACT_SOFTMAX) {
-                        vp = exp_rel(xp, Mp) * iSp;
-                        const A vq = exp_rel(xqq, Mq) * iSq;
-                        a = vp - vq > (A)0 ? vp - vq : (A)0;
-                    } else if (ACT == ACT_SIGMOID) {
-                        // sigma(tp) - sigma(tq) = sigma(tp) sigma(-tq) (1 - e^-(tp-tq)): no cancellation.
-                        const A tp_ = (xp - alpha) * invw, tq_ = (xqq - alpha) * invw;
-                        const A d = (xp - xqq) * invw;
-                        vp = (A)1 / ((A)1 + exp_neg(tp_));
-                        const A sqn = (A)1 / ((A)1 + exp_neg(-tq_));
-                        a = d > (A)0 ? vp * sqn * (-expm1_acc(-d)) : (A)0;
-                    } else {
-                        vp = xp;
-                        a = xp - xqq > (A)0 ? xp - xqq : (A)0;
-                    }
-                    ta += a;
-                    tp += vp;
-                }
-            }
-            out = make_double2(warp_sum((double)ta), warp_sum((double)tp));
+__device__ void get_decision(const StepParams& P, int b, bool write, Shared& sh) {
+    const int tid = threadIdx.x;
+    if (P.sample_mode) {
+        if (tid == 0) {
+            Decision d{};
+            d.mode = MODE_BONUS;
+            d.row = 0;
+            d.Sp = d.Sq = 1.0;
+            sh.dec = d;
         }
+    } else if (ACT == ACT_SOFTMAX) {
+        if (tid == 0) {
+            while (ld_acquire(&P.flag[b]) == 0u) __nanosleep(40);
+            const Decision* dp = &P.dec[b];
+            Decision d;
+            d.mode = __ldcg(&dp->mode);
+            d.row = __ldcg(&dp->row);
+            d.Mp = __ldcg(&dp->Mp);
+            d.Sp = __ldcg(&dp->Sp);
+            d.Mq = __ldcg(&dp->Mq);
+            d.Sq = __ldcg(&dp->Sq);
+            sh.dec = d;
+        }
+    } else if (tid < 32) {
+        decide_gather<T, ACT>(P, b, write, sh.dec);
     }
-    if (lane == 0) ri.gpart[pos * kConsWarps + warp] = out;
-    if (pos != ri.len - 1) return;
-    if (!run_last_warp(ri)) return;
-    const int g0 = ri.q * P.runB * kConsWarps;
-    const int ng = min(ri.len * kConsWarps, P.NG - g0);
-    for (int i = lane; i < ng; i += 32) P.gpart[(size_t)ri.b * P.NG + g0 + i] = ri.gpart[i];
-    __threadfence();
-    __syncwarp();
-    if (lane == 0) {
-        ri.cnt = 0;
-        red_release_add(&P.cnt2[ri.b], 1u);
+    __syncthreads();
+}
+
+// B-item j of batch row b: granules 8j .. 8j+7 of the needed row(s); thread 0
+// publishes the 8 partials, then counts the item (release).
+template <typename T, int ACT>
+__device__ void item_B(const StepParams& P, int b, int j, Shared& sh) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    get_decision<T, ACT>(P, b, false, sh);
+    const Decision d = sh.dec;
+    const int g0 = j * kWarps;
+    if (d.mode != MODE_NONE) {
+        const int g = g0 + warp;
+        double2 gp = make_double2(0.0, 0.0);
+        if (g < P.NG) granule<T, ACT>(P, b, g, d, &gp);
+        if (lane == 0) sh.wpart[warp] = gp;
+        __syncthreads();
+    }
+    if (tid == 0) {
+        if (d.mode != MODE_NONE) {
+            double2* out = P.gpart + (size_t)b * P.NG;
+            for (int w = 0; w < kWarps && g0 + w < P.NG; ++w) out[g0 + w] = sh.wpart[w];
+        }
+        red_release_add(&P.cnt2[b], 1u);
+    }
+}
+
+// L-item of batch row b: waits for the row's B-items, runs the inverse CDF,
+// and leaves b's counters at zero for the next launch.
+template <typename T, int ACT>
+__device__ void item_L(const StepParams& P, int b, Shared& sh, double2* gcache) {
+    const int tid = threadIdx.x;
+    get_decision<T, ACT>(P, b, true, sh);
+    const Decision d = sh.dec;
+    if (tid == 0) wait_geq(&P.cnt2[b], (unsigned)P.nB);
+    __syncthreads();
+    if (d.mode != MODE_NONE) {
+        if (tid == 0) trace(P, 4 * b + 2);
+        locate<T, ACT>(P, b, d, sh, gcache);
+        if (tid == 0) trace(P, 4 * b + 3);
+    }
+    if (tid == 0) {  // every B-item of b has read the flag and been counted
+        P.cnt2[b] = 0;
+        P.flag[b] = 0;
     }
 }
 
 // ---------------------------------------------------------------------------
 template <typename T, int ACT>
-__global__ void __launch_bounds__(kBlock, 2) k_verify(StepParams P) {
-    using A = typename Elem<T>::acc;
-    constexpr int CA = kStageBytes / (int)sizeof(T);
-    extern __shared__ __align__(128) uint8_t smem[];
-    uint8_t* stages = smem;
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)kStages * kStageStride);
-    uint64_t* empty = full + kStages;
-    Slot* slots = reinterpret_cast<Slot*>(empty + kStages);
-    double2* gcache = reinterpret_cast<double2*>(slots + kStages);
-    RunInfo* runs = reinterpret_cast<RunInfo*>(gcache + kLocCap);
-    __shared__ double s_red[kConsWarps];
-    __shared__ int s_ired[kConsWarps];
-    __shared__ double2 s_rs[kMaxRowsSmem];
-
-    if (threadIdx.x == 0) {
-        trace(P, 2 * blockIdx.x);
-        for (int s = 0; s < kStages; ++s) {
-            mbar_init(&full[s], 1);
-            mbar_init(&empty[s], kConsWarps);  // every consumer warp frees the stage
-        }
-        for (int c = 0; c < kCtx; ++c) runs[c].cnt = 0;
-        mbar_fence_init();
+__global__ void __launch_bounds__(kCtaThreads, kCtaMinBlocks) k_verify(StepParams P) {
+    __shared__ Shared sh;
+    extern __shared__ __align__(128) uint4 dsm[];
+    const int tid = threadIdx.x;
+    if (P.trace && blockIdx.x == 0 && tid == 0) trace(P, 4 * P.B);
+    // Claims run two ahead: the item after the current one is known while the
+    // current one runs (an A-run streams its first chunks early), and the
+    // claim after that is in flight.
+    unsigned q1 = 0, q2 = 0;
+    if (tid == 0) {
+        q1 = atomicAdd(P.next, 1u);
+        q2 = atomicAdd(P.next, 1u);
     }
-    __syncthreads();
-
-    if (threadIdx.x >= kCons) {
-        if (threadIdx.x == kCons) producer<T, ACT>(P, stages, full, empty, slots, runs);
-    } else {
-        const int lane = threadIdx.x & 31;
-        LaneRun<A> L{(A)-INFINITY, (A)INFINITY, 0.0};
-        unsigned n = 0;
-        for (;;) {
-            const unsigned s = n % kStages, ph = (n / kStages) & 1u;
-            mbar_wait(&full[s], ph);
-            const int4 hdr = *reinterpret_cast<const int4*>(&slots[s]);  // type, ctx, pos, b
-            ++n;
-            if (hdr.x == IT_STOP) break;
-            const uint8_t* st = stages + (size_t)s * kStageStride;
-            if (hdr.x == IT_A) {
-                RunInfo& ri = runs[hdr.y];
-                const int pos = hdr.z, len = ri.len;
-                const int lo = (ri.k0 + pos) * CA;
-                if (pos == 0) L = LaneRun<A>{(A)-INFINITY, (A)INFINITY, 0.0};
-                chunk_A<T>(P, st, ri.shift_p, min(CA, P.V - lo), L, &empty[s]);
-                if (pos == len - 1) finish_A<A>(P, ri, L);
-            } else if (hdr.x == IT_B) {
-                RunInfo& ri = runs[hdr.y];
-                const int lo = (ri.k0 + hdr.z) * P.CB;
-                chunk_B<T, ACT>(P, ri, st, hdr.z, min(P.CB, P.V - lo), &empty[s]);
+    AStream as;
+    for (;;) {
+        if (tid == 0) {
+            sh.item = q1;
+            sh.item_next = q2;
+            q1 = q2;
+            q2 = atomicAdd(P.next, 1u);
+        }
+        __syncthreads();
+        const unsigned i = sh.item, inext = sh.item_next;
+        if (i >= P.n_items) break;
+        const ItemRef it = decode_item(P, i);
+        if (it.type == IT_B) {
+            item_B<T, ACT>(P, it.b, it.idx, sh);
+        } else if (it.type == IT_L) {
+            item_L<T, ACT>(P, it.b, sh, reinterpret_cast<double2*>(dsm));
+        } else if constexpr (ACT == ACT_SOFTMAX) {
+            if (it.type == IT_A) {
+                const ItemRef nx = inext < P.n_items ? decode_item(P, inext) : ItemRef{-1, 0, 0};
+                item_A<T>(P, it.b, it.idx, nx, sh, dsm, as);
             } else {
-                const Slot sl = slots[s];
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&empty[s]);
-                cbar<kCons>();  // the decide / locate run on the whole consumer group
-                const int tb = 2 * (int)gridDim.x + 4 * sl.b + (sl.type == IT_D ? 0 : 2);
-                if (threadIdx.x == 0) trace(P, tb);
-                if (sl.type == IT_D) {
-                    if (ACT == ACT_SOFTMAX && !P.sample_mode) decide_exact<T>(P, sl.b, s_red, s_ired, s_rs);
-                    else if (threadIdx.x < 32) decide_gather<T, ACT>(P, sl.b);
-                } else {
-                    locate<T, ACT>(P, sl, gcache, s_red, s_ired);
-                }
-                if (threadIdx.x == 0) trace(P, tb + 1);
+                if (tid == 0) trace(P, 4 * it.b);
+                item_D<T>(P, it.b, sh);
+                if (tid == 0) trace(P, 4 * it.b + 1);
             }
         }
+        __syncthreads();  // the item's shared state is dead before the next one
     }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        trace(P, 2 * blockIdx.x + 1);
+    if (tid == 0) {
+        if (P.trace) atomicMax(&P.trace[4 * P.B + 1], gtime());
         __threadfence();
-        const unsigned prev = atomicAdd(P.exit_cnt, 1u);
-        if (prev == gridDim.x - 1) {  // last CTA out resets the work counters
+        if (atomicAdd(P.exit_cnt, 1u) == gridDim.x - 1) {  // last CTA out resets the claim counter
             *P.exit_cnt = 0;
             *P.next = 0;
-            __threadfence();
         }
     }
 }
@@ -1143,92 +1104,122 @@ static int sm_count() {
     return n;
 }
 
-constexpr size_t kVerifySmem = (size_t)kStages * kStageStride + 2 * kStages * sizeof(uint64_t) +
-                               kStages * sizeof(Slot) + kLocCap * sizeof(double2) + kCtx * sizeof(RunInfo);
-
 static size_t elem_size(int dtype) { return dtype == DT_F64 ? 8 : (dtype == DT_BF16 ? 2 : 4); }
 
 void plan_geometry(int dtype, int act, StepParams& P) {
     const int s = (int)elem_size(dtype);
-    const int CA = kStageBytes / s;
-    P.CH = CA;
-    P.CB = kStageBytes / (2 * s);
-    P.GW = P.CB / kConsWarps;
-    P.NG = (P.V + P.GW - 1) / P.GW;
-    P.nBi = (P.V + P.CB - 1) / P.CB;
-    if (P.sample_mode || act != ACT_SOFTMAX) {
+    const int VEC = 16 / s;
+    P.nB = (P.V + kCB - 1) / kCB;
+    P.NG = (P.V + kGW - 1) / kGW;
+    const long resident = (long)sm_count() * kCtaMinBlocks;
+    const bool exact = act == ACT_SOFTMAX && !P.sample_mode;
+    if (!exact) {
         P.NR = 0;
-        P.K = 0;
+        P.Kc = P.runA = P.K = 0;
+        P.nA = 0;
     } else {
-        P.K = (P.V + CA - 1) / CA;
+        // chunks per row (any alignment) and the run length: long enough to
+        // amortize a partial over many chunks, short enough that the A phase
+        // still spreads over ~4 items per resident CTA.
+        const long nvec = (P.V + 2L * VEC - 2) / VEC;
+        const long CV = (long)kCtaThreads * kAVec;
+        P.Kc = (int)((nvec + CV - 1) / CV);
+        // A run of up to 4 chunks (64 KB) takes a few microseconds, so a row's
+        // statistics complete within a few microseconds of its last run's
+        // dispatch and the lags below stay short (in time and in L2 bytes).
+        static const int run_cap = [] {  // experiment knob (SSV_RUNA)
+            const char* e = getenv("SSV_RUNA");
+            return e ? std::max(1, atoi(e)) : 4;
+        }();
+        long want = ((long)P.Kc * P.B * P.NR + 4 * resident - 1) / (4 * resident);
+        want = std::max<long>(1, std::min<long>({want, (long)P.Kc, (long)run_cap}));
+        const long runs = (P.Kc + want - 1) / want;
+        P.runA = (int)((P.Kc + runs - 1) / runs);
+        P.K = (P.Kc + P.runA - 1) / P.runA;
+        P.nA = P.NR * P.K;
     }
-    const long grid = 2L * sm_count();
-    // Runs: long enough to amortize one publish over many 16 KB chunks, short
-    // enough that every phase still spreads over ~4 runs per CTA.
-    auto run_len = [&](long chunks_per_row, long rows, int cap) {
-        if (chunks_per_row <= 0) return 1;
-        long want = (chunks_per_row * rows + 4 * grid - 1) / (4 * grid);
-        want = std::max<long>(1, std::min<long>({want, chunks_per_row, (long)cap}));
-        const long runs = (chunks_per_row + want - 1) / want;
-        return (int)((chunks_per_row + runs - 1) / runs);
-    };
-    P.runA = P.K > 0 ? run_len(P.K, (long)P.B * P.NR, kMaxRunA) : 1;
-    P.RPR = P.K > 0 ? (P.K + P.runA - 1) / P.runA : 0;
-    P.runB = run_len(P.nBi, P.B, kMaxRunB);
-    P.nA = P.NR * P.RPR;
     P.nph[IT_A] = P.nA;
-    P.nph[IT_D] = P.sample_mode ? 0 : 1;
-    P.nph[IT_B] = (P.nBi + P.runB - 1) / P.runB;
+    P.nph[IT_D] = exact ? 1 : 0;
+    P.nph[IT_B] = P.nB;
     P.nph[IT_L] = 1;
+    static const bool a_only = getenv("SSV_AONLY") != nullptr;  // experiment knob: A phase alone (no results)
+    if (a_only && exact) P.nph[IT_D] = P.nph[IT_B] = P.nph[IT_L] = 0;
+    // Phase offsets, in segments of one batch row each: a phase of row b is
+    // dispatched about one resident wave after the phase it waits on, so the
+    // wait is short and the rejected pair (read by the A-items a few rows
+    // earlier) is still in L2 when its B-items re-read it.
+    // items in progress at any time: one per resident CTA plus one claimed ahead
     const long seg = (long)P.nph[0] + P.nph[1] + P.nph[2] + P.nph[3];
-    P.n_items = (unsigned)((long)P.B * seg);
-    const long g = std::min<long>(grid, std::max<long>(1, P.n_items));
-    // Items a CTA may hold: the run in its ring and the one claimed ahead.
-    // Lag between the phases of one batch row, in segments, so a phase's
-    // dependency has completed when a producer reaches it.
-    const long inflight = g * 3;
-    P.claim = 1;
-    P.lag = (int)std::max<long>(1, std::min<long>(P.B, (inflight + seg - 1) / seg + 1));
-    int o = 0;
-    for (int p = 0; p < 4; ++p) {
-        P.off[p] = o;
-        if (P.nph[p] > 0) o += P.lag;
-    }
+    static const int lag_mult = [] {  // experiment knob (SSV_LAG_MULT), default 1
+        const char* e = getenv("SSV_LAG_MULT");
+        return e ? std::max(1, atoi(e)) : 1;
+    }();
+    const int wave = lag_mult * (int)((2 * resident + seg - 1) / seg);
+    auto clampB = [&](long x) { return (int)std::min<long>(P.B, std::max<long>(0, x)); };
+    P.off[IT_A] = 0;
+    P.off[IT_D] = exact ? clampB(wave) : 0;
+    P.off[IT_B] = exact ? clampB(P.off[IT_D] + std::max(1, wave / 2)) : 0;
+    P.off[IT_L] = clampB(P.off[IT_B] + wave);
+    // Ranges of constant segment composition.
     int pts[10], n = 0;
     pts[n++] = 0;
-    const int tend = P.B + P.off[3];
-    pts[n++] = tend;
     for (int p = 0; p < 4; ++p) {
         if (P.nph[p] == 0) continue;
-        pts[n++] = std::min(P.off[p], tend);
-        pts[n++] = std::min(P.off[p] + P.B, tend);
+        pts[n++] = P.off[p];
+        pts[n++] = P.off[p] + P.B;
     }
-    for (int i = 1; i < n; ++i)  // insertion sort of <= 10 points
+    for (int i = 1; i < n; ++i)  // insertion sort of <= 9 points, then dedupe
         for (int j = i; j > 0 && pts[j - 1] > pts[j]; --j) std::swap(pts[j - 1], pts[j]);
-    P.nbp = 0;
+    int m = 0;
     for (int i = 0; i < n; ++i)
-        if (P.nbp == 0 || pts[i] != P.bp[P.nbp - 1]) P.bp[P.nbp++] = pts[i];
+        if (m == 0 || pts[i] != pts[m - 1]) pts[m++] = pts[i];
+    n = m;
+    const int tend = P.B + P.off[IT_L];
+    P.nrange = 0;
+    unsigned item = 0;
+    for (int i = 0; i < n && pts[i] < tend; ++i) {
+        const int t0 = pts[i], t1 = i + 1 < n ? std::min(pts[i + 1], tend) : tend;
+        int sz = 0;
+        for (int p = 0; p < 4; ++p)
+            if (P.nph[p] > 0 && t0 - P.off[p] >= 0 && t0 - P.off[p] < P.B) sz += P.nph[p];
+        if (sz == 0 || t1 <= t0) continue;
+        P.rseg[P.nrange] = t0;
+        P.ritem[P.nrange] = item;
+        P.rsize[P.nrange] = sz;
+        ++P.nrange;
+        item += (unsigned)sz * (unsigned)(t1 - t0);
+    }
+    P.ritem[P.nrange] = item;
+    P.rseg[P.nrange] = tend;
+    P.n_items = item;
 }
 
-int verify_grid(const StepParams& P) { return (int)std::min<long>(2L * sm_count(), std::max<long>(1, P.n_items)); }
+int trace_slots(const StepParams& P) { return 4 * P.B + 2; }
 
 template <typename T, int ACT>
 static void launch_verify_t(const StepParams& P, const Launch& L) {
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(k_verify<T, ACT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kVerifySmem);
+        cudaFuncSetAttribute(k_verify<T, ACT>, cudaFuncAttributeMaxDynamicSharedMemorySize, kDynSmem);
         attr = true;
     }
-    const int grid = (int)std::min<long>(2L * sm_count(), std::max<long>(1, P.n_items));
+    static int per_sm = 0;
+    if (per_sm == 0) {
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_verify<T, ACT>, kCtaThreads, kDynSmem);
+        per_sm = std::max(1, per_sm);
+    }
+    // Persistent: one CTA per resident slot, items claimed in order.  (Any
+    // grid size is deadlock-free -- items only wait on earlier claims.)
+    const unsigned grid = std::min<unsigned>(P.n_items, (unsigned)(sm_count() * per_sm));
     const int h = L.begin(KID_VERIFY);
-    k_verify<T, ACT><<<grid, kBlock, kVerifySmem, L.st>>>(P);
+    k_verify<T, ACT><<<grid, kCtaThreads, kDynSmem, L.st>>>(P);
     L.end(h);
 }
 
 template <typename T, int ACT>
 static void launch_mat_t(const StepParams& P, void* p, void* q, void* r, const Launch& L) {
     const int h = L.begin(KID_MATERIALIZE);
-    k_materialize<T, ACT><<<148 * 8, kThreads, 0, L.st>>>(P, p, q, r);
+    k_materialize<T, ACT><<<sm_count() * 8, kThreads, 0, L.st>>>(P, p, q, r);
     L.end(h);
 }
 
@@ -1260,7 +1251,7 @@ void launch_sample_softmax(int dtype, const StepParams& P, const Launch& L) {
 }
 
 void launch_gen_logits(int dtype, uint64_t seed, int B, int G, int V, void* zp, void* zq, const Launch& L) {
-    const int blocks = 148 * 16;
+    const int blocks = sm_count() * 16;
     const int h = L.begin(KID_GEN);
     if (dtype == DT_F32) k_gen_logits<float><<<blocks, kThreads, 0, L.st>>>(seed, B, G, V, (float*)zp, (float*)zq);
     else if (dtype == DT_BF16)

@@ -14,17 +14,27 @@ enum DType : int { DT_F32 = SSV_F32, DT_BF16 = SSV_BF16, DT_F64 = SSV_F64 };
 enum Act : int { ACT_SOFTMAX = 0, ACT_SIGMOID = 1, ACT_PROBS = 2 };
 enum Mode : int { MODE_NONE = 0, MODE_REJECT = 1, MODE_BONUS = 2 };
 
-// Persistent-kernel geometry: a ring of kStages shared-memory stages of
-// kStageBytes each, filled by TMA bulk copies.  A-items (row statistics) take
-// one chunk of kStageBytes; B-items (the rejected pair / bonus row) take half a
-// stage per row; one consumer warp owns one granule (B-item / 8) of a B-item.
-constexpr int kStages = 4;
-constexpr int kStageBytes = 16384;
-constexpr int kStageStride = kStageBytes + 64;  // room for the 16-byte-aligned superset
-constexpr int kHalfStride = kStageStride / 2;   // 16-byte aligned
-constexpr int kLocCap = 1024;                   // granule partials cached in SMEM by locate
+// Work-item geometry of k_verify (one CTA of kCtaThreads threads per item):
+//   A-item  a run of runA consecutive 16 KB chunks (16-byte aligned) of one
+//           statistics row, streamed through a kAStages-deep cp.async ring of
+//           per-thread shared-memory slots (kAVec 16-byte vectors per thread
+//           per chunk).
+//   D-item  the decision of one batch row (exact only).
+//   B-item  kCB consecutive elements of the rejected row pair (or the bonus
+//           row) of one batch row; warp w of the CTA owns granule w of kGW
+//           elements.
+//   L-item  the inverse CDF (locate) of one batch row.
+constexpr int kCtaThreads = 256;
+constexpr int kWarpsPerCta = kCtaThreads / 32;
+constexpr int kAVec = 4;                                 // 16-byte vectors per thread per chunk
+constexpr int kAStages = 4;                              // cp.async ring depth
+constexpr int kAChunkBytes = kCtaThreads * kAVec * 16;   // 16 KB
+constexpr int kDynSmem = kAStages * kAChunkBytes;        // 64 KB (aliased by locate's granule cache)
+constexpr int kCB = 4096;
+constexpr int kGW = kCB / (kCtaThreads / 32);  // 512
+constexpr int kLocCap = 1024;                  // granule partials a locate caches in SMEM
 
-// What batch row b still needs after the acceptance scan (K1 -> K2).
+// What batch row b still needs after the acceptance scan (decide -> B-items).
 struct Decision {
     int mode;  // Mode
     int row;   // rejected position c*, or gamma for the bonus row
@@ -37,34 +47,34 @@ struct StepParams {
     const void* zq;
     const int32_t* ids;
     const double* u;
-    int B, G, V, PS;  // batch, gamma, vocab, p steps (gamma or gamma+1)
-    int NR, K, CH;    // stat rows per batch row, A-chunks per row, A-chunk elements
-    int NG;           // granules per row
-    int CB, GW;       // B-item elements per row, granule elements (CB / 8)
-    int nA, nBi, lag; // per batch row: A-items, B-items; lag = segments between a row's A- and D-items
-    int nph[4];       // items per batch row of each phase (A, D, B, L)
-    int off[4];       // segment offset of each phase
-    int bp[9], nbp;   // sorted segment breakpoints (piecewise-constant segment sizes)
-    int claim;        // items claimed per atomic by a producer
-    int runA, RPR;    // chunks per A-run, A-runs (= partials) per stat row
-    int runB;         // slices per B-run
-    unsigned long long* trace;  // diagnostics: [2*grid] CTA start/end, [4*B] decide/locate start/end
-    unsigned n_items;
-    unsigned epoch;   // per-launch tag of the decision flags (never reset)
+    int B, G, V, PS;   // batch, gamma, vocab, p steps (gamma or gamma+1)
+    int NR;            // statistics rows per batch row (0: no A phase)
+    int Kc;            // 16 KB chunks per statistics row (any alignment)
+    int runA;          // chunks per A-item
+    int K;             // A-items (= partials) per statistics row
+    int nA, nB;        // A- and B-items per batch row
+    int NG;            // granules per row
+    int nph[4];        // items per batch row of each phase (A, D, B, L)
+    int off[4];        // segment offset of each phase: segment t holds phase p of row t - off[p]
+    int nrange;        // segment ranges of constant composition
+    int rseg[9];       // first segment of each range (+ end)
+    unsigned ritem[9]; // first item of each range (+ total)
+    int rsize[8];      // items per segment in each range
+    unsigned n_items;  // grid size
     double alpha, width;
-    int sample_mode;    // K2 only: sample softmax(z_p row b) with u[b] (draft sampling)
-    int check_uniforms; // StepInputs::validate checks u in [0,1); the sigmoid variant does not
+    int sample_mode;     // sample softmax(z_p row b) with u[b] (draft sampling)
+    int check_uniforms;  // StepInputs::validate checks u in [0,1); the sigmoid variant does not
+    unsigned long long* trace;  // diagnostics: [4*B] decide/locate start/end, [4*B..+2) kernel start/end
     // scratch
-    double2* part;     // [B][NR][RPR] run partials (max, sum e^(x-max))
-    double2* rowstat;  // [B][NR]     row (max, sum)
+    double2* part;     // [B][NR][K][8] A-item warp partials (max, sum e^(x-max))
+    double2* rowstat;  // [B][NR]    row (max, sum)
     Decision* dec;     // [B]
-    double2* gpart;    // [B][NG]     granule partials
-    double* gat;       // [B][NR]     logit at the drafted token of each stat row
-    unsigned* cnt1;    // [B] self-resetting completion counters (A-items)
-    unsigned* cnt2;    // [B]                                      (B-items)
-    unsigned* flag;    // [B] decision published (== epoch)
-    unsigned* next;    // [1] work counter, reset by the last CTA to exit
-    unsigned* exit_cnt;// [1]
+    double2* gpart;    // [B][NG]    granule partials
+    unsigned* next;     // [1] item claim counter   (reset by the last CTA to exit)
+    unsigned* exit_cnt; // [1] CTAs done            (reset by the last CTA to exit)
+    unsigned* cnt1;    // [B] A-items done       (reset by the D-item)
+    unsigned* cnt2;    // [B] B-items done       (reset by the L-item)
+    unsigned* flag;    // [B] decision published (reset by the L-item)
     // outputs
     int32_t* acc;
     int32_t* fin;
@@ -105,7 +115,7 @@ struct Launch {
 };
 
 void plan_geometry(int dtype, int act, StepParams& P);
-int verify_grid(const StepParams& P);
+int trace_slots(const StepParams& P);
 void launch_verify(int dtype, int act, const StepParams& P, void* outp, void* outq, void* outr,
                    const Launch& L);
 void launch_sample_softmax(int dtype, const StepParams& P, const Launch& L);

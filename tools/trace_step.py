@@ -23,7 +23,7 @@ run = (lambda: v.verify_exact(zp, zq, ids, u)) if a.variant == "exact" else (lam
 for _ in range(3):
     run()
 torch.cuda.synchronize()
-cap = 2 * 296 + 4 * a.B
+cap = 4 * a.B + 2
 v.trace_enable(cap)
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 s = torch.cuda.Stream()
@@ -34,17 +34,13 @@ with torch.cuda.stream(s):
     e1.record(s)
 s.synchronize()
 t = v.trace_read(cap).astype(np.int64)
-grid = 296
-cta = t[: 2 * grid].reshape(grid, 2)
-cta = cta[cta[:, 0] > 0]
-t0 = cta[:, 0].min()
-print(f"event ms {e0.elapsed_time(e1) * 1e3:.1f} us; kernel span {(cta[:, 1].max() - t0) / 1e3:.1f} us; "
-      f"CTA start spread {(cta[:, 0].max() - t0) / 1e3:.1f} us; CTA end min {(cta[:, 1].min() - t0) / 1e3:.1f} us")
-ph = t[2 * grid: 2 * grid + 4 * a.B].reshape(a.B, 4)
+t0, t1 = t[4 * a.B], t[4 * a.B + 1]
+print(f"event {e0.elapsed_time(e1) * 1e3:.1f} us; kernel span (CTA 0 start -> last CTA end) {(t1 - t0) / 1e3:.1f} us")
+ph = t[: 4 * a.B].reshape(a.B, 4)
 acc = r.accepted_len.cpu().numpy()
+f = lambda x: f"{(x - t0) / 1e3:7.1f}" if x > 0 else "      -"
 for b in range(min(a.B, 16)):
-    f = lambda x: f"{(x - t0) / 1e3:7.1f}" if x > 0 else "      -"
     print(f"b={b:3d} acc={acc[b]} D {f(ph[b, 0])} -> {f(ph[b, 1])}   L {f(ph[b, 2])} -> {f(ph[b, 3])}")
 if a.B > 16:
-    valid = ph[:, 0] > 0
-    print("D start max", (ph[valid, 0].max() - t0) / 1e3, "L end max", (ph[ph[:, 3] > 0, 3].max() - t0) / 1e3)
+    for b in range(16, a.B, max(1, a.B // 16)):
+        print(f"b={b:3d} acc={acc[b]} D {f(ph[b, 0])} -> {f(ph[b, 1])}   L {f(ph[b, 2])} -> {f(ph[b, 3])}")
