@@ -418,7 +418,10 @@ __device__ void item_D(const StepParams& P, int b, Shared& sh) {
         zq = load_exact(q_row<T>(P, b, tid) + x);
     }
     if (tid <= G) u = P.u[(size_t)b * (G + 1) + tid];
-    if (tid == 0) wait_geq(&P.cnt1[b], (unsigned)P.nA * kWarps);
+    if (tid == 0) {
+        wait_geq(&P.cnt1[b], (unsigned)P.nA * kWarps);
+        trace(P, 8 * b + 1);
+    }
     __syncthreads();
     const int KP = P.K * kWarps;  // partials per statistics row
     for (int r = warp; r < P.NR; r += kWarps) {
@@ -893,7 +896,9 @@ __device__ void get_decision(const StepParams& P, int b, bool write, Shared& sh)
 template <typename T, int ACT>
 __device__ void item_B(const StepParams& P, int b, int j, Shared& sh) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (j == 0 && tid == 0) trace(P, 8 * b + 3);
     get_decision<T, ACT>(P, b, false, sh);
+    if (j == 0 && tid == 0) trace(P, 8 * b + 4);
     const Decision d = sh.dec;
     const int g0 = j * kWarps;
     if (d.mode != MODE_NONE) {
@@ -917,14 +922,17 @@ __device__ void item_B(const StepParams& P, int b, int j, Shared& sh) {
 template <typename T, int ACT>
 __device__ void item_L(const StepParams& P, int b, Shared& sh, double2* gcache) {
     const int tid = threadIdx.x;
+    if (tid == 0) trace(P, 8 * b + 5);
     get_decision<T, ACT>(P, b, true, sh);
     const Decision d = sh.dec;
-    if (tid == 0) wait_geq(&P.cnt2[b], (unsigned)P.nB);
+    if (tid == 0) {
+        wait_geq(&P.cnt2[b], (unsigned)P.nB);
+        trace(P, 8 * b + 6);
+    }
     __syncthreads();
     if (d.mode != MODE_NONE) {
-        if (tid == 0) trace(P, 4 * b + 2);
         locate<T, ACT>(P, b, d, sh, gcache);
-        if (tid == 0) trace(P, 4 * b + 3);
+        if (tid == 0) trace(P, 8 * b + 7);
     }
     if (tid == 0) {  // every B-item of b has read the flag and been counted
         P.cnt2[b] = 0;
@@ -938,7 +946,7 @@ __global__ void __launch_bounds__(kCtaThreads, kCtaMinBlocks) k_verify(StepParam
     __shared__ Shared sh;
     extern __shared__ __align__(128) uint4 dsm[];
     const int tid = threadIdx.x;
-    if (P.trace && blockIdx.x == 0 && tid == 0) trace(P, 4 * P.B);
+    if (P.trace && blockIdx.x == 0 && tid == 0) trace(P, 8 * P.B);
     // Claims run two ahead: the item after the current one is known while the
     // current one runs (an A-run streams its first chunks early), and the
     // claim after that is in flight.
@@ -968,15 +976,15 @@ __global__ void __launch_bounds__(kCtaThreads, kCtaMinBlocks) k_verify(StepParam
                 const ItemRef nx = inext < P.n_items ? decode_item(P, inext) : ItemRef{-1, 0, 0};
                 item_A<T>(P, it.b, it.idx, nx, sh, dsm, as);
             } else {
-                if (tid == 0) trace(P, 4 * it.b);
+                if (tid == 0) trace(P, 8 * it.b);
                 item_D<T>(P, it.b, sh);
-                if (tid == 0) trace(P, 4 * it.b + 1);
+                if (tid == 0) trace(P, 8 * it.b + 2);
             }
         }
         __syncthreads();  // the item's shared state is dead before the next one
     }
     if (tid == 0) {
-        if (P.trace) atomicMax(&P.trace[4 * P.B + 1], gtime());
+        if (P.trace) atomicMax(&P.trace[8 * P.B + 1], gtime());
         __threadfence();
         if (atomicAdd(P.exit_cnt, 1u) == gridDim.x - 1) {  // last CTA out resets the claim counter
             *P.exit_cnt = 0;
@@ -1124,12 +1132,13 @@ void plan_geometry(int dtype, int act, StepParams& P) {
         const long nvec = (P.V + 2L * VEC - 2) / VEC;
         const long CV = (long)kCtaThreads * kAVec;
         P.Kc = (int)((nvec + CV - 1) / CV);
-        // A run of up to 4 chunks (64 KB) takes a few microseconds, so a row's
-        // statistics complete within a few microseconds of its last run's
-        // dispatch and the lags below stay short (in time and in L2 bytes).
+        // Runs as long as load balance allows (up to 64 chunks = 1 MB): every
+        // run ends in a warp fold and a claim, so long runs keep the ring busy
+        // (measured: 38-chunk runs stream at ~100% of the copy roofline, 4-chunk
+        // runs at ~70%).  The lags below scale with the run length.
         static const int run_cap = [] {  // experiment knob (SSV_RUNA)
             const char* e = getenv("SSV_RUNA");
-            return e ? std::max(1, atoi(e)) : 4;
+            return e ? std::max(1, atoi(e)) : 64;
         }();
         long want = ((long)P.Kc * P.B * P.NR + 4 * resident - 1) / (4 * resident);
         want = std::max<long>(1, std::min<long>({want, (long)P.Kc, (long)run_cap}));
@@ -1150,16 +1159,19 @@ void plan_geometry(int dtype, int act, StepParams& P) {
     // earlier) is still in L2 when its B-items re-read it.
     // items in progress at any time: one per resident CTA plus one claimed ahead
     const long seg = (long)P.nph[0] + P.nph[1] + P.nph[2] + P.nph[3];
-    static const int lag_mult = [] {  // experiment knob (SSV_LAG_MULT), default 1
+    static const int lag_mult = [] {  // experiment knob (SSV_LAG_MULT), default by run length
         const char* e = getenv("SSV_LAG_MULT");
-        return e ? std::max(1, atoi(e)) : 1;
+        return e ? std::max(1, atoi(e)) : 0;
     }();
-    const int wave = lag_mult * (int)((2 * resident + seg - 1) / seg);
+    const int wave = (int)((2 * resident + seg - 1) / seg);
+    // A D-item waits for its row's runs, which take ~runA/8 "waves" of
+    // claims to complete; B- and L-items follow one wave after that.
+    const int mD = lag_mult ? lag_mult : std::max(1, (P.runA + 7) / 8);
     auto clampB = [&](long x) { return (int)std::min<long>(P.B, std::max<long>(0, x)); };
     P.off[IT_A] = 0;
-    P.off[IT_D] = exact ? clampB(wave) : 0;
-    P.off[IT_B] = exact ? clampB(P.off[IT_D] + std::max(1, wave / 2)) : 0;
-    P.off[IT_L] = clampB(P.off[IT_B] + wave);
+    P.off[IT_D] = exact ? clampB((long)mD * wave) : 0;
+    P.off[IT_B] = exact ? clampB(P.off[IT_D] + (long)std::max(1, mD / 2) * wave) : 0;
+    P.off[IT_L] = clampB(P.off[IT_B] + (long)std::max(1, mD) * wave);
     // Ranges of constant segment composition.
     int pts[10], n = 0;
     pts[n++] = 0;
@@ -1194,7 +1206,7 @@ void plan_geometry(int dtype, int act, StepParams& P) {
     P.n_items = item;
 }
 
-int trace_slots(const StepParams& P) { return 4 * P.B + 2; }
+int trace_slots(const StepParams& P) { return 8 * P.B + 2; }
 
 template <typename T, int ACT>
 static void launch_verify_t(const StepParams& P, const Launch& L) {

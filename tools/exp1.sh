@@ -6,8 +6,7 @@ run() { # name env...
   python -c "
 import json;d=json.load(open('$OUT/exp_$name.json'));print('$name', round(d['roofline']['kernel_ms']*1e3,1),'us', round(d['roofline']['frac'],3))" >> $OUT/exp_summary.txt 2>&1
 }
-for r in 4 8 16 38; do run pm_r$r SSV_RUNA=$r SSV_LAG_MULT=1000; done
-for r in 8 16; do run full_r${r}_m3 SSV_RUNA=$r SSV_LAG_MULT=3; done
-WL=c3; for r in 1 2 4 8; do run c3_pm_r${r} SSV_RUNA=$r SSV_LAG_MULT=1000; done
-WL=c3bf16; for r in 2 4 8; do run c3b_pm_r${r} SSV_RUNA=$r SSV_LAG_MULT=1000; done
-WL=c2; for r in 1 2; do run c2_pm_r${r} SSV_RUNA=$r SSV_LAG_MULT=1000; done
+for r in 12 16 24 38; do for m in 2 3 4 6; do run c4_r${r}_m$m SSV_RUNA=$r SSV_LAG_MULT=$m; done; done
+WL=c3; for r in 2 4 8; do for m in 1 2 3; do run c3_r${r}_m$m SSV_RUNA=$r SSV_LAG_MULT=$m; done; done
+WL=c3bf16; for r in 4 8; do for m in 1 2 3; do run c3b_r${r}_m$m SSV_RUNA=$r SSV_LAG_MULT=$m; done; done
+WL=c2; for r in 1 2; do for m in 1 2; do run c2_r${r}_m$m SSV_RUNA=$r SSV_LAG_MULT=$m; done; done
