@@ -178,6 +178,7 @@ int run_device(ssv_ctx* ctx, int variant, const ssv_verify_args* a, ssv_verify_o
     P.width = a->beta - a->alpha;
     P.check_uniforms = variant != V_SIGMOID;
     plan_geometry(a->dtype, variant, P);
+    plan_cluster(a->dtype, variant, P);
     const Layout L = plan_scratch(P, 0);
     rc = ensure_scratch(ctx, L.total, (size_t)P.B);
     if (rc) return rc;

@@ -33,12 +33,15 @@
 // (optional p / q / residual grids) and the synthetic-input generator follow.
 #include <algorithm>
 #include <cfloat>
+#include <cstdio>
 #include <cstdlib>
 #include <type_traits>
 
 #include "ssv_launch.h"
 #include "ssv_device.cuh"
 #include "ssv_pipe.cuh"
+
+#include <cooperative_groups.h>
 
 namespace ssv {
 
@@ -717,14 +720,16 @@ __device__ void granule(const StepParams& P, int b, int g, const Decision& d, do
 // granule prefix (contiguous ownership, one scan) -> exact fp64 scan inside
 // the selected granule (dist.cpp:122-137, incl. both fallbacks).
 template <typename T, int ACT>
-__device__ void locate(const StepParams& P, int b, const Decision& d, Shared& sh, double2* gcache) {
+__device__ void locate(const StepParams& P, int b, const Decision& d, Shared& sh, double2* gcache,
+                       bool cached = false) {
     const int NG = P.NG, GW = kGW;
-    const double2* gp = P.gpart + (size_t)b * NG;
+    const double2* gp = P.gpart + (size_t)b * NG;  // (cached: gcache already holds all NG <= kLocCap)
     const T* pr = p_row<T>(P, b, d.row);
     const T* qr = d.mode == MODE_REJECT ? q_row<T>(P, b, d.row) : nullptr;
     const double u = __ldcg(&P.u[(size_t)b * (P.G + 1) + P.G]);  // u_final, verify_reference.cpp:98
     const int ncache = min(NG, kLocCap);
-    for (int g = threadIdx.x; g < ncache; g += kCtaThreads) gcache[g] = __ldcg(&gp[g]);
+    if (!cached)
+        for (int g = threadIdx.x; g < ncache; g += kCtaThreads) gcache[g] = __ldcg(&gp[g]);
     __syncthreads();
     auto raw = [&](int g) -> double2 { return g < kLocCap ? gcache[g] : __ldcg(&gp[g]); };
 
@@ -994,6 +999,247 @@ __global__ void __launch_bounds__(kCtaThreads, kCtaMinBlocks) k_verify(StepParam
 }
 
 // ---------------------------------------------------------------------------
+// K1c/K2c k_verify_cluster<T, ACT>: the small-batch path.  One
+// thread-block cluster of cl_size CTAs per batch row; rank k owns the element
+// slice [k*SE, (k+1)*SE) of every row:
+//   1. exact: one TMA bulk copy per drafted p / q row stages the rank's slice of
+//      the row in a ring of cl_slots shared-memory slots (all rows at once when
+//      they fit), while all threads gather the drafted logits and the
+//      uniforms; one warp per row folds the slice to (max, sum e^(x - max)) as
+//      it lands (FMNMX3; fp32 pairs of <= 16 terms, fp64 across) and restages
+//      the slot it consumed with a later row;
+//   2. cluster barrier; every CTA folds the cl_size slice partials of every row
+//      through DSMEM in the same fixed order, so all ranks reach the identical
+//      decision (tau in fp64, first rejection) without another exchange;
+//      sigmoid / probabilities: the decision comes from the gathers alone;
+//   3. each rank reduces its slice of the rejected pair / bonus row (L2-hot) to
+//      512-element granule masses;
+//   4. cluster barrier; rank 0 gathers the granule masses through DSMEM and runs
+//      the inverse CDF (locate).
+template <typename T, int ACT>
+__global__ void __launch_bounds__(kCtaThreads, 1) k_verify_cluster(StepParams P) {
+    namespace cg = cooperative_groups;
+    constexpr int VEC = Elem<T>::VEC;
+    constexpr bool EXACT = ACT == ACT_SOFTMAX;
+    cg::cluster_group cl = cg::this_cluster();
+    __shared__ Shared sh;
+    extern __shared__ __align__(128) uint8_t csm[];
+    const int CS = P.cl_size, SE = P.cl_se, GPS = P.cl_gps, RB = P.cl_rowbytes;
+    const int rank = (int)cl.block_rank();
+    const int b = blockIdx.x / CS;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int G = P.G, V = P.V;
+    const int e0 = min(V, rank * SE), n = min(V, e0 + SE) - e0;  // this rank's slice
+    const int NRc = EXACT ? P.cl_rows : 0;
+    const int NS = EXACT ? P.cl_slots : 1;  // ring slots (NS == NRc: every row resident at once)
+    // shared-memory carve-up (host: cluster_smem)
+    uint8_t* slots = csm;                                                       // NS x RB
+    uint64_t* full = reinterpret_cast<uint64_t*>(slots + (size_t)NS * RB);      // NS (even-padded)
+    double2* part = reinterpret_cast<double2*>(full + ((NS + 1) & ~1));         // [NRc] slice partials (DSMEM)
+    double2* gloc = part + NRc;                                                 // [GPS] granule partials (DSMEM)
+    double2* gcache = gloc + GPS;                                               // [NG] rank 0: all granules
+    double* zg = reinterpret_cast<double*>(gcache + P.NG);                     // [3G + 1] gathers, uniforms
+    int* offs = reinterpret_cast<int*>(zg + 3 * G + 1);                         // [NS]
+
+    const bool tr = P.trace && rank == 0 && tid == 0;  // per-row stamps (tools/trace_step.py)
+    if (tr) {
+        trace(P, 8 * b);
+        if (b == 0) trace(P, 8 * P.B);
+    }
+    auto stage_row = [&](int r) {  // thread 0: bulk-copy the 16-byte superset of row r's slice into slot r % NS
+        const int sl = r % NS;
+        const T* row = r < G ? p_row<T>(P, b, r) : (r < 2 * G ? q_row<T>(P, b, r - G) : p_row<T>(P, b, G));
+        const uintptr_t a0 = reinterpret_cast<uintptr_t>(row + e0), a1 = reinterpret_cast<uintptr_t>(row + e0 + n);
+        const uintptr_t s0 = a0 & ~uintptr_t(15), s1 = (a1 + 15) & ~uintptr_t(15);
+        offs[sl] = (int)((a0 - s0) / sizeof(T));
+        mbar_arrive_expect_tx(&full[sl], (uint32_t)(s1 - s0));
+        bulk_g2s(slots + (size_t)sl * RB, reinterpret_cast<const void*>(s0), (uint32_t)(s1 - s0), &full[sl]);
+    };
+    const bool tx = tr && b == 0;  // finer stamps for batch row 0: trace[8B + 2 + k]
+    if (EXACT && tid == 0) {
+        for (int i = 0; i < NS; ++i) mbar_init(&full[i], 1);
+        mbar_fence_init();
+        if (n > 0)
+            for (int r = 0; r < NS; ++r) stage_row(r);
+    }
+    if (tx) trace(P, 8 * P.B + 2);
+    // gathers and uniforms (needed by every rank for the decision)
+    for (int c = tid; c < G; c += kCtaThreads) {
+        int x = P.ids[(size_t)b * G + c];
+        if (x < 0 || x >= V) {
+            if (rank == 0) flag(P, SSV_STATUS_TOKEN_RANGE);
+            x = x < 0 ? 0 : V - 1;
+        }
+        zg[c] = load_exact(p_row<T>(P, b, c) + x);
+        zg[G + c] = load_exact(q_row<T>(P, b, c) + x);
+    }
+    for (int c = tid; c <= G; c += kCtaThreads) {
+        const double u = P.u[(size_t)b * (G + 1) + c];
+        zg[2 * G + c] = u;
+        if (rank == 0 && P.check_uniforms && (!(u >= 0.0) || !(u < 1.0))) flag(P, SSV_STATUS_UNIFORM_RANGE);
+    }
+    __syncthreads();
+    if (tx) trace(P, 8 * P.B + 3);
+
+    if constexpr (EXACT) {
+        // One warp per row slice (rows in flight in parallel): max, then
+        // sum e^(x - max) over the slice, fp32 pairs of <= 16 terms, fp64
+        // across.  The warp that consumed a slot restages it with row r + NS.
+        float mn = FLT_MAX;
+        for (int r = warp; r < NRc; r += kWarps) {
+            const int sl = r % NS;
+            float m = -FLT_MAX;
+            double sd = 0.0;
+            if (n > 0) {
+                mbar_wait(&full[sl], (unsigned)(r / NS) & 1u);
+                const bool txw = P.trace && rank == 0 && b == 0 && lane == 0;
+                if (txw && r < 8) trace(P, 8 * P.B + 4 + r);
+                const int off = offs[sl], nv = (off + n + VEC - 1) / VEC;
+                const uint4* rv = reinterpret_cast<const uint4*>(slots + (size_t)sl * RB);
+                auto load = [&](int v) {
+                    uint4 w = rv[v];
+                    if (v == 0 && off) mask_vec<T>(w, off, VEC);
+                    if (v == nv - 1 && (off + n) % VEC) mask_vec<T>(w, 0, (off + n) % VEC);
+                    return w;
+                };
+                // 4 vectors per step (independent shared-memory loads in flight)
+                const uint4 padv = pad_vec<T>();
+                for (int v0 = lane; v0 < nv; v0 += 128) {
+                    uint4 w[4];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) w[u] = v0 + 32 * u < nv ? load(v0 + 32 * u) : padv;
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) AStat<T>::minmax(w[u], m, mn);
+                }
+                m = warp_max(m);
+                if (m != -FLT_MAX) {
+                    const float2 negM = make_float2(-m, -m);
+                    for (int v0 = lane; v0 < nv; v0 += 128) {
+                        uint4 w[4];
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) w[u] = v0 + 32 * u < nv ? load(v0 + 32 * u) : padv;
+                        float2 s0 = make_float2(0.f, 0.f), s1 = make_float2(0.f, 0.f);
+                        AStat<T>::expsum(w[0], negM, s0);
+                        AStat<T>::expsum(w[1], negM, s1);
+                        AStat<T>::expsum(w[2], negM, s0);
+                        AStat<T>::expsum(w[3], negM, s1);  // <= 16 fp32 terms per pair lane, then fp64
+                        sd += ((double)s0.x + (double)s0.y) + ((double)s1.x + (double)s1.y);
+                    }
+                }
+                __syncwarp();
+                if (txw && r < 6) trace(P, 8 * P.B + 12 + r);
+                if (lane == 0 && r + NS < NRc) stage_row(r + NS);  // this warp was the slot's only reader
+            }
+            const double S = warp_sum(sd);
+            if (lane == 0) {
+                if (isnan(S) || m == INFINITY) flag(P, SSV_STATUS_NONFINITE);
+                part[r] = S != 0.0 ? make_double2((double)m, S) : make_double2(-CUDART_INF, 0.0);
+            }
+        }
+        if (__any_sync(kFull, isinf(mn)) && lane == 0) flag(P, SSV_STATUS_NONFINITE);
+        if (tr) trace(P, 8 * b + 1);
+        cl.sync();  // slice partials visible to the cluster
+        if (tr) trace(P, 8 * b + 2);
+        for (int r = warp; r < NRc; r += kWarps) {
+            double2 v = make_double2(-CUDART_INF, 0.0);
+            if (lane < CS) v = *cl.map_shared_rank(&part[r], lane);
+            const double M = warp_max(v.x);
+            const double S = warp_sum(v.y != 0.0 ? v.y * exp(v.x - M) : 0.0);  // NaN propagates
+            if (lane == 0) {
+                if (!isfinite(M) || !isfinite(S)) flag(P, SSV_STATUS_NONFINITE);
+                if (r < kMaxRowsSmem) sh.rs[r] = make_double2(M, S);
+                if (rank == 0 && r < P.NR) P.rowstat[(size_t)b * P.NR + r] = make_double2(M, S);
+            }
+        }
+        __syncthreads();
+    }
+    // decision (warp 0; every rank computes the same one)
+    if (warp == 0) {
+        int accepted = G;
+        for (int c0 = 0; c0 < G; c0 += 32) {
+            const int c = c0 + lane;
+            bool rej = false;
+            if (c < G) {
+                double p, q;
+                if (EXACT) {
+                    const double2 sp = sh.rs[c], sq = sh.rs[G + c];
+                    p = exp(zg[c] - sp.x) / sp.y;  // activation.cpp:20-27, dist.cpp:46-50
+                    q = exp(zg[G + c] - sq.x) / sq.y;
+                } else if (ACT == ACT_SIGMOID) {
+                    p = sigmoid_scaled_d(zg[c], P.alpha, P.width);  // dist.cpp:60-62
+                    q = sigmoid_scaled_d(zg[G + c], P.alpha, P.width);
+                } else {
+                    p = zg[c];
+                    q = zg[G + c];
+                    if (rank == 0 && (p < 0.0 || q < 0.0)) flag(P, SSV_STATUS_NEGATIVE);
+                }
+                const double tau = ratio_clamped(p, q);
+                if (rank == 0) P.tau[(size_t)b * G + c] = tau;
+                rej = !(zg[2 * G + c] <= tau);  // verify_reference.cpp:93-96 (inclusive)
+            }
+            const unsigned msk = __ballot_sync(kFull, rej);
+            if (msk && accepted == G) accepted = c0 + __ffs(msk) - 1;
+        }
+        if (lane == 0) {
+            Decision dd{};
+            dd.Sp = dd.Sq = 1.0;
+            if (accepted < G) {
+                dd.mode = MODE_REJECT;
+                dd.row = accepted;
+                if (EXACT) {
+                    dd.Mp = sh.rs[accepted].x;
+                    dd.Sp = sh.rs[accepted].y;
+                    dd.Mq = sh.rs[G + accepted].x;
+                    dd.Sq = sh.rs[G + accepted].y;
+                }
+            } else if (P.PS == G + 1) {
+                dd.mode = MODE_BONUS;
+                dd.row = G;
+            } else {
+                dd.mode = MODE_NONE;
+            }
+            sh.dec = dd;
+            if (rank == 0) {
+                P.acc[b] = accepted;
+                if (dd.mode == MODE_NONE) {
+                    P.fin[b] = -1;  // kNoToken, step.hpp:11
+                    P.rsu[b] = 0;
+                    P.rden[b] = 0.0;
+                }
+            }
+        }
+    }
+    __syncthreads();
+    if (tr) trace(P, 8 * b + 3);
+    const Decision d = sh.dec;
+    // granule masses of this rank's slice of the needed row(s) (L2-hot re-read)
+    if (d.mode != MODE_NONE)
+        for (int j = warp; j < GPS; j += kWarps) {
+            const int g = rank * GPS + j;
+            double2 out = make_double2(0.0, 0.0);
+            if (g < P.NG) granule<T, ACT>(P, b, g, d, &out);
+            if (lane == 0) gloc[j] = out;
+        }
+    if (tr) trace(P, 8 * b + 4);
+    cl.sync();  // granule masses visible to rank 0 (and every DSMEM read of `part` is done)
+    if (tr) trace(P, 8 * b + 5);
+    if (d.mode == MODE_NONE) return;
+    if (rank == 0)
+        for (int g = tid; g < P.NG; g += kCtaThreads) {
+            const int k = g / GPS, j = g - k * GPS;
+            gcache[g] = *cl.map_shared_rank(&gloc[j], k);
+        }
+    cl.sync();  // rank 0 is done reading the others' shared memory
+    if (rank != 0) return;
+    if (tr) trace(P, 8 * b + 6);
+    locate<T, ACT>(P, b, d, sh, gcache, /*cached=*/true);
+    if (tr) {
+        trace(P, 8 * b + 7);
+        atomicMax(&P.trace[8 * P.B + 1], gtime());
+    }
+}
+
+// ---------------------------------------------------------------------------
 // K3: optional materialized grids (activation.cpp:20-49; verify_fused.cpp:50
 // residual-in-q semantics; verify_sigmoid.cpp:39-48).
 template <typename T, int ACT>
@@ -1206,7 +1452,7 @@ void plan_geometry(int dtype, int act, StepParams& P) {
     P.n_items = item;
 }
 
-int trace_slots(const StepParams& P) { return 8 * P.B + 2; }
+int trace_slots(const StepParams& P) { return 8 * P.B + 18; }
 
 template <typename T, int ACT>
 static void launch_verify_t(const StepParams& P, const Launch& L) {
@@ -1228,6 +1474,120 @@ static void launch_verify_t(const StepParams& P, const Launch& L) {
     L.end(h);
 }
 
+// Cluster path geometry (cl_size 0 = not applicable: use the streaming kernel).
+constexpr int kClusterSmemMax = 227 * 1024 - 4096;  // dynamic budget (static Shared + slack)
+
+constexpr int kClusterSmemTwoPerSm = 100 * 1024;  // two CTAs per SM (twice the resident clusters)
+
+static int cluster_smem(const StepParams& P, int s, int NRc, int NS, int SE, int GPS) {
+    const int VEC = 16 / s;
+    const int RB = ((SE + 2 * VEC) * s + 15) & ~15;
+    long bytes = (long)NS * RB + 8L * ((NS + 1) & ~1) + 16L * (NRc + GPS + P.NG) + 8L * (3 * P.G + 1) + 4L * NS + 64;
+    return bytes > kClusterSmemMax ? -1 : (int)bytes;
+}
+
+template <typename T, int ACT>
+static int max_active_clusters(int cs, int smem) {
+    static int cached_cs = -1, cached_smem = -1, cached = 0;
+    if (cs == cached_cs && smem == cached_smem) return cached;
+    auto k = k_verify_cluster<T, ACT>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, kClusterSmemMax);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(cs, 1, 1);
+    cfg.blockDim = dim3(kCtaThreads, 1, 1);
+    cfg.dynamicSmemBytes = smem;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = cs;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, k, &cfg) != cudaSuccess) {
+        cudaGetLastError();
+        n = 0;
+    }
+    cached_cs = cs;
+    cached_smem = smem;
+    cached = n;
+    return n;
+}
+
+// Small batches: one cluster per batch row, all clusters resident at once.
+// Largest cluster (most SMs per row) whose slices fit in shared memory and of
+// which B fit on the GPU together.
+template <typename T, int ACT>
+static bool plan_cluster_t(StepParams& P, int s) {
+    static const bool off = getenv("SSV_NO_CLUSTER") != nullptr;  // experiment knob
+    static const bool dbg = getenv("SSV_DEBUG") != nullptr;
+    if (off || P.sample_mode || P.G > 256 || P.NG > kLocCap) return false;
+    const int NRc = ACT == ACT_SOFTMAX ? 2 * P.G + (P.NR > 2 * P.G ? 1 : 0) : 0;  // bonus stats only if materialized
+    for (int cs : {16, 12, 8}) {
+        const int SE = ((P.V + cs - 1) / cs + kGW - 1) / kGW * kGW;
+        const int GPS = SE / kGW;
+        const int RB = NRc > 0 ? ((SE + 2 * (16 / s)) * s + 15) & ~15 : 0;
+        // every row resident if that still leaves two CTAs per SM, else a ring
+        int NS = NRc;
+        if (NS > 0 && cluster_smem(P, s, NRc, NS, SE, GPS) > kClusterSmemTwoPerSm) {
+            const int base = cluster_smem(P, s, NRc, 0, SE, GPS);
+            NS = std::max(2, std::min(NRc, (kClusterSmemTwoPerSm - base) / std::max(RB + 20, 1)));
+        }
+        const int smem = cluster_smem(P, s, NRc, NS, SE, GPS);
+        if (smem < 0) continue;
+        const int mac = max_active_clusters<T, ACT>(cs, smem);
+        if (dbg)
+            fprintf(stderr, "ssv: cluster plan act=%d B=%d V=%d rows=%d slots=%d cs=%d SE=%d smem=%d max_active=%d\n",
+                    ACT, P.B, P.V, NRc, NS, cs, SE, smem, mac);
+        if (mac < P.B) continue;
+        P.cl_size = cs;
+        P.cl_se = SE;
+        P.cl_gps = GPS;
+        P.cl_rows = NRc;
+        P.cl_slots = NS;
+        P.cl_rowbytes = RB;
+        P.cl_smem = smem;
+        if (ACT == ACT_SOFTMAX) P.NR = NRc;  // rowstat rows the cluster path writes
+        return true;
+    }
+    return false;
+}
+
+bool plan_cluster(int dtype, int act, StepParams& P) {
+    P.cl_size = 0;
+    if (dtype == DT_F32) {
+        if (act == ACT_SOFTMAX) return plan_cluster_t<float, ACT_SOFTMAX>(P, 4);
+        if (act == ACT_SIGMOID) return plan_cluster_t<float, ACT_SIGMOID>(P, 4);
+        return plan_cluster_t<float, ACT_PROBS>(P, 4);
+    }
+    if (dtype == DT_BF16) {
+        if (act == ACT_SOFTMAX) return plan_cluster_t<__nv_bfloat16, ACT_SOFTMAX>(P, 2);
+        if (act == ACT_SIGMOID) return plan_cluster_t<__nv_bfloat16, ACT_SIGMOID>(P, 2);
+        return plan_cluster_t<__nv_bfloat16, ACT_PROBS>(P, 2);
+    }
+    return false;
+}
+
+template <typename T, int ACT>
+static void launch_cluster_t(const StepParams& P, const Launch& L) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(P.B * P.cl_size), 1, 1);
+    cfg.blockDim = dim3(kCtaThreads, 1, 1);
+    cfg.dynamicSmemBytes = P.cl_smem;
+    cfg.stream = L.st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = P.cl_size;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    const int h = L.begin(KID_VERIFY);
+    cudaLaunchKernelEx(&cfg, k_verify_cluster<T, ACT>, P);
+    L.end(h);
+}
+
 template <typename T, int ACT>
 static void launch_mat_t(const StepParams& P, void* p, void* q, void* r, const Launch& L) {
     const int h = L.begin(KID_MATERIALIZE);
@@ -1235,17 +1595,25 @@ static void launch_mat_t(const StepParams& P, void* p, void* q, void* r, const L
     L.end(h);
 }
 
+template <typename T, int ACT>
+static void launch_step_t(const StepParams& P, const Launch& L) {
+    if constexpr (sizeof(T) != 8) {
+        if (P.cl_size > 0) return launch_cluster_t<T, ACT>(P, L);
+    }
+    launch_verify_t<T, ACT>(P, L);
+}
+
 template <typename T>
 static void dispatch_verify(int act, const StepParams& P, void* outp, void* outq, void* outr, const Launch& L) {
     const bool mat = outp || outq || outr;
     if (act == ACT_SOFTMAX) {
-        launch_verify_t<T, ACT_SOFTMAX>(P, L);
+        launch_step_t<T, ACT_SOFTMAX>(P, L);
         if (mat) launch_mat_t<T, ACT_SOFTMAX>(P, outp, outq, outr, L);
     } else if (act == ACT_SIGMOID) {
-        launch_verify_t<T, ACT_SIGMOID>(P, L);
+        launch_step_t<T, ACT_SIGMOID>(P, L);
         if (mat) launch_mat_t<T, ACT_SIGMOID>(P, outp, outq, outr, L);
     } else {
-        launch_verify_t<T, ACT_PROBS>(P, L);
+        launch_step_t<T, ACT_PROBS>(P, L);
         if (mat) launch_mat_t<T, ACT_PROBS>(P, outp, outq, outr, L);
     }
 }

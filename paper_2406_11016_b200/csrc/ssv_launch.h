@@ -61,6 +61,10 @@ struct StepParams {
     unsigned ritem[9]; // first item of each range (+ total)
     int rsize[8];      // items per segment in each range
     unsigned n_items;  // grid size
+    // Cluster path (small batches, see k_verify_cluster): one cluster of cl_size
+    // CTAs per batch row, rank k stages elements [k*cl_se, (k+1)*cl_se) of every
+    // row it needs in its shared memory.
+    int cl_size, cl_se, cl_gps, cl_rows, cl_slots, cl_rowbytes, cl_smem;
     double alpha, width;
     int sample_mode;     // sample softmax(z_p row b) with u[b] (draft sampling)
     int check_uniforms;  // StepInputs::validate checks u in [0,1); the sigmoid variant does not
@@ -115,6 +119,7 @@ struct Launch {
 };
 
 void plan_geometry(int dtype, int act, StepParams& P);
+bool plan_cluster(int dtype, int act, StepParams& P);  // small-batch cluster path (sets cl_*)
 int trace_slots(const StepParams& P);
 void launch_verify(int dtype, int act, const StepParams& P, void* outp, void* outq, void* outr,
                    const Launch& L);

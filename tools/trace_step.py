@@ -23,7 +23,7 @@ run = (lambda: v.verify_exact(zp, zq, ids, u)) if a.variant == "exact" else (lam
 for _ in range(3):
     run()
 torch.cuda.synchronize()
-cap = 8 * a.B + 2
+cap = 8 * a.B + 18
 v.trace_enable(cap)
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 s = torch.cuda.Stream()
@@ -36,7 +36,8 @@ s.synchronize()
 t = v.trace_read(cap).astype(np.int64)
 t0, t1 = t[8 * a.B], t[8 * a.B + 1]
 print(f"event {e0.elapsed_time(e1) * 1e3:.1f} us; kernel span (CTA 0 start -> last CTA end) {(t1 - t0) / 1e3:.1f} us")
-print("row acc | D claimed stats published | B0 claimed decided | L claimed ready end   (us from kernel start)")
+print("streaming: row acc | D claimed stats published | B0 claimed decided | L claimed ready end")
+print("cluster:   row acc | start stats sync1 | decided granules | sync2 gathered locate-end  (us from kernel start)")
 ph = t[: 8 * a.B].reshape(a.B, 8)
 acc = r.accepted_len.cpu().numpy()
 f = lambda x: f"{(x - t0) / 1e3:6.1f}" if x > 0 else "     -"
@@ -44,3 +45,6 @@ rows = list(range(min(a.B, 16))) + (list(range(16, a.B, max(1, a.B // 16))) if a
 for b in rows:
     p = ph[b]
     print(f"b={b:3d} {acc[b]} | D {f(p[0])} {f(p[1])} {f(p[2])} | B {f(p[3])} {f(p[4])} | L {f(p[5])} {f(p[6])} {f(p[7])}")
+ex = t[8 * a.B + 2: 8 * a.B + 18]
+if ex[0] > 0:
+    print("row-0 fine stamps (us):", " ".join(f"{(x - t0) / 1e3:.1f}" if x > 0 else "-" for x in ex))
