@@ -1096,35 +1096,45 @@ __global__ void __launch_bounds__(kCtaThreads, 1) k_verify_cluster(StepParams P)
                 if (txw && r < 8) trace(P, 8 * P.B + 4 + r);
                 const int off = offs[sl], nv = (off + n + VEC - 1) / VEC;
                 const uint4* rv = reinterpret_cast<const uint4*>(slots + (size_t)sl * RB);
-                auto load = [&](int v) {
+                // Interior vectors [1, nv - 1) in the main loops, unmasked, four
+                // independent accumulator chains per lane (the loops are latency-
+                // bound at 8 warps per SM); the two edge vectors are masked apart.
+                auto edge = [&](int v) {
                     uint4 w = rv[v];
                     if (v == 0 && off) mask_vec<T>(w, off, VEC);
                     if (v == nv - 1 && (off + n) % VEC) mask_vec<T>(w, 0, (off + n) % VEC);
                     return w;
                 };
-                // 4 vectors per step (independent shared-memory loads in flight)
-                const uint4 padv = pad_vec<T>();
-                for (int v0 = lane; v0 < nv; v0 += 128) {
-                    uint4 w[4];
+                const int vi1 = max(1, nv - 1);
+                float mk[4] = {-FLT_MAX, -FLT_MAX, -FLT_MAX, -FLT_MAX}, nk[4] = {FLT_MAX, FLT_MAX, FLT_MAX, FLT_MAX};
+                if (!(P.dbg & 1)) {
+                    for (int v0 = 1 + lane; v0 < vi1; v0 += 128) {
 #pragma unroll
-                    for (int u = 0; u < 4; ++u) w[u] = v0 + 32 * u < nv ? load(v0 + 32 * u) : padv;
-#pragma unroll
-                    for (int u = 0; u < 4; ++u) AStat<T>::minmax(w[u], m, mn);
-                }
-                m = warp_max(m);
-                if (m != -FLT_MAX) {
-                    const float2 negM = make_float2(-m, -m);
-                    for (int v0 = lane; v0 < nv; v0 += 128) {
-                        uint4 w[4];
-#pragma unroll
-                        for (int u = 0; u < 4; ++u) w[u] = v0 + 32 * u < nv ? load(v0 + 32 * u) : padv;
-                        float2 s0 = make_float2(0.f, 0.f), s1 = make_float2(0.f, 0.f);
-                        AStat<T>::expsum(w[0], negM, s0);
-                        AStat<T>::expsum(w[1], negM, s1);
-                        AStat<T>::expsum(w[2], negM, s0);
-                        AStat<T>::expsum(w[3], negM, s1);  // <= 16 fp32 terms per pair lane, then fp64
-                        sd += ((double)s0.x + (double)s0.y) + ((double)s1.x + (double)s1.y);
+                        for (int u = 0; u < 4; ++u)
+                            if (v0 + 32 * u < vi1) AStat<T>::minmax(rv[v0 + 32 * u], mk[u], nk[u]);
                     }
+                    if (lane == 0) AStat<T>::minmax(edge(0), mk[0], nk[0]);
+                    if (lane == 1 && nv > 1) AStat<T>::minmax(edge(nv - 1), mk[1], nk[1]);
+                }
+                m = fmaxf(fmaxf(mk[0], mk[1]), fmaxf(mk[2], mk[3]));
+                mn = fminf(mn, fminf(fminf(nk[0], nk[1]), fminf(nk[2], nk[3])));
+                m = warp_max(m);
+                if (m != -FLT_MAX && !(P.dbg & 2)) {
+                    const float2 negM = make_float2(-m, -m);
+                    for (int v0 = 1 + lane; v0 < vi1; v0 += 128) {
+                        float2 sk[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
+                                        make_float2(0.f, 0.f)};
+#pragma unroll
+                        for (int u = 0; u < 4; ++u)
+                            if (v0 + 32 * u < vi1) AStat<T>::expsum(rv[v0 + 32 * u], negM, sk[u]);
+                        // fp32 tree over the <= 16 terms of this step, then one fp64 add per pair lane
+                        const float2 t = __fadd2_rn(__fadd2_rn(sk[0], sk[1]), __fadd2_rn(sk[2], sk[3]));
+                        sd += (double)t.x + (double)t.y;
+                    }
+                    float2 se = make_float2(0.f, 0.f);
+                    if (lane == 0) AStat<T>::expsum(edge(0), negM, se);
+                    if (lane == 1 && nv > 1) AStat<T>::expsum(edge(nv - 1), negM, se);
+                    sd += (double)se.x + (double)se.y;
                 }
                 __syncwarp();
                 if (txw && r < 6) trace(P, 8 * P.B + 12 + r);
@@ -1548,6 +1558,8 @@ static bool plan_cluster_t(StepParams& P, int s) {
         P.cl_slots = NS;
         P.cl_rowbytes = RB;
         P.cl_smem = smem;
+        static const int dbgm = getenv("SSV_DBG_MODE") ? atoi(getenv("SSV_DBG_MODE")) : 0;
+        P.dbg = dbgm;
         if (ACT == ACT_SOFTMAX) P.NR = NRc;  // rowstat rows the cluster path writes
         return true;
     }
