@@ -128,15 +128,19 @@ class ClockSampler:
 
 # ----------------------------------------------------------------------------- device arm
 class Workload:
-    def __init__(self, v, key, rank, variant, rotate=True):
+    def __init__(self, v, key, rank, variant, rotate=True, world=1):
         import torch
+
+        from paper_2406_11016_b200.shard import shard_range, slab_seed
 
         desc, B, gamma, V, storage = WORKLOADS[key]
         self.key, self.desc, self.B, self.gamma, self.V, self.storage = key, desc, B, gamma, V, storage
         self.variant = variant
         self.s = BYTES[storage]
         tdt = {"f32": torch.float32, "bf16": torch.bfloat16}[storage]
-        zp, zq, ids, u = v.make_bench_inputs(1 + rank * B, B, gamma, V, tdt)
+        # weak scaling: B rows per GPU, global row b seeded 1 + b (bench.cpp:46-74)
+        lo, hi = shard_range(world * B, world, rank)
+        zp, zq, ids, u = v.make_bench_inputs(slab_seed(1, lo), hi - lo, gamma, V, tdt)
         torch.cuda.synchronize()
         self.set_bytes = (zp.numel() + zq.numel()) * self.s
         l2 = torch.cuda.get_device_properties(torch.cuda.current_device()).L2_cache_size
@@ -407,21 +411,17 @@ def main():
 
     v = Verifier(local)
     peak, peak_src = load_peaks()
-    wl = Workload(v, args.workload, rank, args.variant)
+    wl = Workload(v, args.workload, rank, args.variant, world=world)
     sampler = ClockSampler(local)
     m = measure_device(v, wl, args.steps, args.warmup, world, sampler)
     step_bytes, k_bytes, A = wl.algorithmic_bytes(m["result"])
 
     e2e_t, h2d, d2h, e2e_launches = measure_e2e(v, wl, max(3, min(args.steps, 50)), 3)
 
-    def allmax(x):
-        if world == 1:
-            return x
-        import torch.distributed as dist
+    from paper_2406_11016_b200.shard import allmax as _allmax
 
-        t = torch.tensor([x], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
+    def allmax(x):
+        return _allmax(x, device="cuda")
 
     ms = allmax(m["ms_per_step"])
     e2e_t = allmax(e2e_t)
