@@ -46,6 +46,7 @@
 namespace ssv {
 
 constexpr int kMaxRowsSmem = 96;  // row statistics a decide keeps in SMEM (gamma <= 47)
+constexpr int kBG = 2;            // granules per warp per B-item (a B-item covers kBG * 4096 elements per row)
 constexpr int kCtaMinBlocks = 3;  // resident CTAs per SM (64 KB ring each)
 static_assert(kLocCap * sizeof(double2) <= (size_t)kDynSmem, "granule cache aliases the ring");
 
@@ -57,6 +58,7 @@ struct Shared {
     unsigned item, item_next;
     Decision dec;
     double2 wpart[kWarps];
+    double2 gpart2[kWarps * kBG];
     double2 rs[kMaxRowsSmem];
 };
 
@@ -631,88 +633,108 @@ __device__ __forceinline__ double exact_value(const StepParams& P, const RowCtx&
 }
 
 // ---------------------------------------------------------------------------
-// B-item granule: warp w reduces granule j*8 + w of the needed row(s) (coalesced
-// element loads; rows of odd length have arbitrary alignment) to
+// Granules: a warp reduces one 512-element granule of the needed row(s)
+// (coalesced element loads; rows of odd length have arbitrary alignment) to
 //   reject:  (sum max(0, p - q), sum p)          -- residual / fallback masses
 //   bonus:   (max, sum e^(x - max)) [softmax]  or  (0, sum value)
-template <typename T, int ACT>
-__device__ void granule(const StepParams& P, int b, int g, const Decision& d, double2* gp) {
+// Split into load and reduce so a B-item can keep two granules' loads in flight.
+template <typename T>
+struct GranuleData {
     using A = typename Elem<T>::acc;
-    constexpr int EPL = kGW / 32;  // elements per lane per row (16)
+    static constexpr int EPL = kGW / 32;  // elements per lane per row (16)
+    A xs[EPL], xq[EPL];
+    int n;
+};
+
+template <typename T>
+__device__ __forceinline__ void granule_load(const StepParams& P, int b, int g, const Decision& d, GranuleData<T>& D) {
+    using A = typename Elem<T>::acc;
     const int lane = threadIdx.x & 31;
-    const int lo = g * kGW, n = min(kGW, P.V - lo);
+    const int lo = g * kGW;
+    D.n = g < P.NG ? min(kGW, P.V - lo) : 0;
     const bool reject = d.mode == MODE_REJECT;
     const T* pr = p_row<T>(P, b, d.row) + lo;
     const T* qr = reject ? q_row<T>(P, b, d.row) + lo : pr;
-    const A alpha = (A)P.alpha, invw = (A)(1.0 / P.width);
-    A xs[EPL], xq[EPL];
 #pragma unroll
-    for (int t = 0; t < EPL; ++t) {
+    for (int t = 0; t < GranuleData<T>::EPL; ++t) {
         const int e = t * 32 + lane;
-        xs[t] = e < n ? load_elem(pr + e) : (A)0;
-        xq[t] = (reject && e < n) ? load_elem(qr + e) : (A)0;
+        D.xs[t] = e < D.n ? load_elem(pr + e) : (A)0;
+        D.xq[t] = (reject && e < D.n) ? load_elem(qr + e) : (A)0;
     }
-    double2 out;
-    if (!reject) {
+}
+
+template <typename T, int ACT>
+__device__ __forceinline__ double2 granule_reduce(const StepParams& P, const Decision& d, const GranuleData<T>& D) {
+    using A = typename Elem<T>::acc;
+    constexpr int EPL = GranuleData<T>::EPL;
+    const int lane = threadIdx.x & 31;
+    const int n = D.n;
+    const A alpha = (A)P.alpha, invw = (A)(1.0 / P.width);
+    if (d.mode != MODE_REJECT) {
         if (ACT == ACT_SOFTMAX) {
             A mx = -INFINITY, mn = INFINITY;
 #pragma unroll
             for (int t = 0; t < EPL; ++t)
                 if (t * 32 + lane < n) {
-                    mx = fmax(mx, xs[t]);
-                    mn = fmin(mn, xs[t]);
+                    mx = fmax(mx, D.xs[t]);
+                    mn = fmin(mn, D.xs[t]);
                 }
             mx = warp_max(mx);
             mn = warp_min(mn);
             A sm = 0;
 #pragma unroll
             for (int t = 0; t < EPL; ++t)
-                if (t * 32 + lane < n) sm += exp_rel(xs[t], mx);
+                if (t * 32 + lane < n) sm += exp_rel(D.xs[t], mx);
             const double S = warp_sum((double)sm);
-            if (lane == 0 && (!isfinite((double)mx) || isnan(S) || !isfinite((double)mn)))
+            if (n > 0 && lane == 0 && (!isfinite((double)mx) || isnan(S) || !isfinite((double)mn)))
                 flag(P, SSV_STATUS_NONFINITE);
-            out = make_double2((double)mx, S);
-        } else {
-            A sm = 0;
-#pragma unroll
-            for (int t = 0; t < EPL; ++t) {
-                if (t * 32 + lane < n) {
-                    if (ACT == ACT_SIGMOID) sm += (A)1 / ((A)1 + exp_neg((xs[t] - alpha) * invw));
-                    else sm += xs[t];
-                }
-            }
-            out = make_double2(0.0, warp_sum((double)sm));
+            return make_double2((double)mx, S);
         }
-    } else {
-        const A Mp = (A)d.Mp, Mq = (A)d.Mq, iSp = (A)(1.0 / d.Sp), iSq = (A)(1.0 / d.Sq);
-        A ta = 0, tp = 0;
+        A sm = 0;
 #pragma unroll
         for (int t = 0; t < EPL; ++t) {
             if (t * 32 + lane < n) {
-                const A xp = xs[t], xqq = xq[t];
-                A a, vp;
-                if (ACT == ACT_SOFTMAX) {
-                    vp = exp_rel(xp, Mp) * iSp;
-                    const A vq = exp_rel(xqq, Mq) * iSq;
-                    a = vp - vq > (A)0 ? vp - vq : (A)0;
-                } else if (ACT == ACT_SIGMOID) {
-                    // sigma(tp) - sigma(tq) = sigma(tp) sigma(-tq) (1 - e^-(tp-tq)): no cancellation.
-                    const A tp_ = (xp - alpha) * invw, tq_ = (xqq - alpha) * invw;
-                    const A dd = (xp - xqq) * invw;
-                    vp = (A)1 / ((A)1 + exp_neg(tp_));
-                    const A sqn = (A)1 / ((A)1 + exp_neg(-tq_));
-                    a = dd > (A)0 ? vp * sqn * (-expm1_acc(-dd)) : (A)0;
-                } else {
-                    vp = xp;
-                    a = xp - xqq > (A)0 ? xp - xqq : (A)0;
-                }
-                ta += a;
-                tp += vp;
+                if (ACT == ACT_SIGMOID) sm += (A)1 / ((A)1 + exp_neg((D.xs[t] - alpha) * invw));
+                else sm += D.xs[t];
             }
         }
-        out = make_double2(warp_sum((double)ta), warp_sum((double)tp));
+        return make_double2(0.0, warp_sum((double)sm));
     }
-    if (lane == 0) *gp = out;
+    const A Mp = (A)d.Mp, Mq = (A)d.Mq, iSp = (A)(1.0 / d.Sp), iSq = (A)(1.0 / d.Sq);
+    A ta = 0, tp = 0;
+#pragma unroll
+    for (int t = 0; t < EPL; ++t) {
+        if (t * 32 + lane < n) {
+            const A xp = D.xs[t], xqq = D.xq[t];
+            A a, vp;
+            if (ACT == ACT_SOFTMAX) {
+                vp = exp_rel(xp, Mp) * iSp;
+                const A vq = exp_rel(xqq, Mq) * iSq;
+                a = vp - vq > (A)0 ? vp - vq : (A)0;
+            } else if (ACT == ACT_SIGMOID) {
+                // sigma(tp) - sigma(tq) = sigma(tp) sigma(-tq) (1 - e^-(tp-tq)): no cancellation.
+                const A tp_ = (xp - alpha) * invw, tq_ = (xqq - alpha) * invw;
+                const A dd = (xp - xqq) * invw;
+                vp = (A)1 / ((A)1 + exp_neg(tp_));
+                const A sqn = (A)1 / ((A)1 + exp_neg(-tq_));
+                a = dd > (A)0 ? vp * sqn * (-expm1_acc(-dd)) : (A)0;
+            } else {
+                vp = xp;
+                a = xp - xqq > (A)0 ? xp - xqq : (A)0;
+            }
+            ta += a;
+            tp += vp;
+        }
+    }
+    return make_double2(warp_sum((double)ta), warp_sum((double)tp));
+}
+
+template <typename T, int ACT>
+__device__ void granule(const StepParams& P, int b, int g, const Decision& d, double2* gp) {
+    GranuleData<T> D;
+    granule_load<T>(P, b, g, d, D);
+    const double2 out = granule_reduce<T, ACT>(P, d, D);
+    if ((threadIdx.x & 31) == 0) *gp = out;
 }
 
 // ---------------------------------------------------------------------------
@@ -863,9 +885,8 @@ __device__ void locate(const StepParams& P, int b, const Decision& d, Shared& sh
     if (threadIdx.x == 0) P.fin[b] = token;
 }
 
-// The decision a B- or L-item works from.  Exact: wait for the D-item's
-// release flag.  Sampling: the bonus row is row 0.  Sigmoid / probabilities:
-// recompute it from the gathered values (warp 0; the L-item writes outputs).
+// The decision a B- or L-item works from: the D-item's (release flag), or,
+// when sampling, the bonus row 0.
 template <typename T, int ACT>
 __device__ void get_decision(const StepParams& P, int b, bool write, Shared& sh) {
     const int tid = threadIdx.x;
@@ -877,7 +898,7 @@ __device__ void get_decision(const StepParams& P, int b, bool write, Shared& sh)
             d.Sp = d.Sq = 1.0;
             sh.dec = d;
         }
-    } else if (ACT == ACT_SOFTMAX) {
+    } else {
         if (tid == 0) {
             while (ld_acquire(&P.flag[b]) == 0u) __nanosleep(40);
             const Decision* dp = &P.dec[b];
@@ -890,14 +911,29 @@ __device__ void get_decision(const StepParams& P, int b, bool write, Shared& sh)
             d.Sq = __ldcg(&dp->Sq);
             sh.dec = d;
         }
-    } else if (tid < 32) {
-        decide_gather<T, ACT>(P, b, write, sh.dec);
     }
+    (void)write;
     __syncthreads();
 }
 
-// B-item j of batch row b: granules 8j .. 8j+7 of the needed row(s); thread 0
-// publishes the 8 partials, then counts the item (release).
+// Sigmoid / probability D-item: the decision from the gathered values alone
+// (warp 0, paper section 3.2.2), published like the exact one.
+template <typename T, int ACT>
+__device__ void item_D_gather(const StepParams& P, int b, Shared& sh) {
+    if (threadIdx.x >= 32) return;
+    if (threadIdx.x == 0) trace(P, 8 * b);
+    decide_gather<T, ACT>(P, b, true, sh.dec);
+    __syncwarp();
+    if (threadIdx.x == 0) {
+        P.dec[b] = sh.dec;
+        st_release(&P.flag[b], 1u);
+        trace(P, 8 * b + 2);
+    }
+}
+
+// B-item j of batch row b: granules kBG*8*j .. +kBG*8-1 of the needed row(s),
+// kBG per warp with both granules' loads in flight; thread 0 publishes the
+// partials, then counts the item (release).
 template <typename T, int ACT>
 __device__ void item_B(const StepParams& P, int b, int j, Shared& sh) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -905,18 +941,22 @@ __device__ void item_B(const StepParams& P, int b, int j, Shared& sh) {
     get_decision<T, ACT>(P, b, false, sh);
     if (j == 0 && tid == 0) trace(P, 8 * b + 4);
     const Decision d = sh.dec;
-    const int g0 = j * kWarps;
+    const int g0 = j * kWarps * kBG;
     if (d.mode != MODE_NONE) {
-        const int g = g0 + warp;
-        double2 gp = make_double2(0.0, 0.0);
-        if (g < P.NG) granule<T, ACT>(P, b, g, d, &gp);
-        if (lane == 0) sh.wpart[warp] = gp;
+        GranuleData<T> D[kBG];
+#pragma unroll
+        for (int k = 0; k < kBG; ++k) granule_load<T>(P, b, g0 + k * kWarps + warp, d, D[k]);
+#pragma unroll
+        for (int k = 0; k < kBG; ++k) {
+            const double2 gp = granule_reduce<T, ACT>(P, d, D[k]);
+            if (lane == 0) sh.gpart2[k * kWarps + warp] = gp;
+        }
         __syncthreads();
     }
     if (tid == 0) {
         if (d.mode != MODE_NONE) {
             double2* out = P.gpart + (size_t)b * P.NG;
-            for (int w = 0; w < kWarps && g0 + w < P.NG; ++w) out[g0 + w] = sh.wpart[w];
+            for (int w = 0; w < kWarps * kBG && g0 + w < P.NG; ++w) out[g0 + w] = sh.gpart2[w];
         }
         red_release_add(&P.cnt2[b], 1u);
     }
@@ -955,18 +995,24 @@ __global__ void __launch_bounds__(kCtaThreads, kCtaMinBlocks) k_verify(StepParam
     // Claims run two ahead: the item after the current one is known while the
     // current one runs (an A-run streams its first chunks early), and the
     // claim after that is in flight.
+    // (With few items per CTA the claim-ahead would hand two items to half the
+    // CTAs and none to the rest: then claim one at a time.)
     unsigned q1 = 0, q2 = 0;
     if (tid == 0) {
         q1 = atomicAdd(P.next, 1u);
-        q2 = atomicAdd(P.next, 1u);
+        q2 = P.claim_ahead ? atomicAdd(P.next, 1u) : P.n_items;
     }
     AStream as;
     for (;;) {
         if (tid == 0) {
             sh.item = q1;
             sh.item_next = q2;
-            q1 = q2;
-            q2 = atomicAdd(P.next, 1u);
+            if (P.claim_ahead) {
+                q1 = q2;
+                q2 = atomicAdd(P.next, 1u);
+            } else {
+                q1 = atomicAdd(P.next, 1u);
+            }
         }
         __syncthreads();
         const unsigned i = sh.item, inext = sh.item_next;
@@ -985,6 +1031,8 @@ __global__ void __launch_bounds__(kCtaThreads, kCtaMinBlocks) k_verify(StepParam
                 item_D<T>(P, it.b, sh);
                 if (tid == 0) trace(P, 8 * it.b + 2);
             }
+        } else {
+            item_D_gather<T, ACT>(P, it.b, sh);  // (the only other item type without an A phase)
         }
         __syncthreads();  // the item's shared state is dead before the next one
     }
@@ -1373,7 +1421,7 @@ static size_t elem_size(int dtype) { return dtype == DT_F64 ? 8 : (dtype == DT_B
 void plan_geometry(int dtype, int act, StepParams& P) {
     const int s = (int)elem_size(dtype);
     const int VEC = 16 / s;
-    P.nB = (P.V + kCB - 1) / kCB;
+    P.nB = (P.V + kCB * kBG - 1) / (kCB * kBG);
     P.NG = (P.V + kGW - 1) / kGW;
     const long resident = (long)sm_count() * kCtaMinBlocks;
     const bool exact = act == ACT_SOFTMAX && !P.sample_mode;
@@ -1404,7 +1452,7 @@ void plan_geometry(int dtype, int act, StepParams& P) {
         P.nA = P.NR * P.K;
     }
     P.nph[IT_A] = P.nA;
-    P.nph[IT_D] = exact ? 1 : 0;
+    P.nph[IT_D] = P.sample_mode ? 0 : 1;  // exact: row statistics + decision; sigmoid / probs: gathers only
     P.nph[IT_B] = P.nB;
     P.nph[IT_L] = 1;
     static const bool a_only = getenv("SSV_AONLY") != nullptr;  // experiment knob: A phase alone (no results)
@@ -1425,9 +1473,15 @@ void plan_geometry(int dtype, int act, StepParams& P) {
     const int mD = lag_mult ? lag_mult : std::max(1, (P.runA + 7) / 8);
     auto clampB = [&](long x) { return (int)std::min<long>(P.B, std::max<long>(0, x)); };
     P.off[IT_A] = 0;
-    P.off[IT_D] = exact ? clampB((long)mD * wave) : 0;
-    P.off[IT_B] = exact ? clampB(P.off[IT_D] + (long)std::max(1, mD / 2) * wave) : 0;
-    P.off[IT_L] = clampB(P.off[IT_B] + (long)std::max(1, mD) * wave);
+    if (exact) {
+        P.off[IT_D] = clampB((long)mD * wave);
+        P.off[IT_B] = clampB(P.off[IT_D] + (long)std::max(1, mD / 2) * wave);
+        P.off[IT_L] = clampB(P.off[IT_B] + (long)std::max(1, mD) * wave);
+    } else {  // a gathers-only D-item takes ~2 us: B-items one wave later, L one wave after them
+        P.off[IT_D] = 0;
+        P.off[IT_B] = P.sample_mode ? 0 : clampB(wave);
+        P.off[IT_L] = clampB(P.off[IT_B] + wave);
+    }
     // Ranges of constant segment composition.
     int pts[10], n = 0;
     pts[n++] = 0;
@@ -1479,8 +1533,10 @@ static void launch_verify_t(const StepParams& P, const Launch& L) {
     // Persistent: one CTA per resident slot, items claimed in order.  (Any
     // grid size is deadlock-free -- items only wait on earlier claims.)
     const unsigned grid = std::min<unsigned>(P.n_items, (unsigned)(sm_count() * per_sm));
+    StepParams Q = P;
+    Q.claim_ahead = P.n_items > 2u * grid;
     const int h = L.begin(KID_VERIFY);
-    k_verify<T, ACT><<<grid, kCtaThreads, kDynSmem, L.st>>>(P);
+    k_verify<T, ACT><<<grid, kCtaThreads, kDynSmem, L.st>>>(Q);
     L.end(h);
 }
 

@@ -60,7 +60,8 @@ struct StepParams {
     int rseg[9];       // first segment of each range (+ end)
     unsigned ritem[9]; // first item of each range (+ total)
     int rsize[8];      // items per segment in each range
-    unsigned n_items;  // grid size
+    unsigned n_items;  // work items
+    int claim_ahead;   // claim the next item before processing the current one (set at launch)
     // Cluster path (small batches, see k_verify_cluster): one cluster of cl_size
     // CTAs per batch row, rank k stages elements [k*cl_se, (k+1)*cl_se) of every
     // row it needs in its shared memory.
