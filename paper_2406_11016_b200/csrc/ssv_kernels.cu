@@ -50,6 +50,10 @@ constexpr int kBG = 2;            // granules per warp per B-item (a B-item cove
 constexpr int kCtaMinBlocks = 3;  // resident CTAs per SM (64 KB ring each)
 static_assert(kLocCap * sizeof(double2) <= (size_t)kDynSmem, "granule cache aliases the ring");
 
+struct ItemRef {
+    int type, b, idx;
+};
+
 struct Shared {
     float fred[kWarps];
     double dred[kWarps];
@@ -104,9 +108,6 @@ __device__ __forceinline__ double ratio_clamped(double p, double q) {  // dist.c
 // smaller block indices.  The segment composition is piecewise constant over
 // at most 8 ranges the host tabulates.
 enum ItemType : int { IT_A = 0, IT_D = 1, IT_B = 2, IT_L = 3 };
-struct ItemRef {
-    int type, b, idx;
-};
 
 __device__ __forceinline__ ItemRef decode_item(const StepParams& P, unsigned i) {
     int k = 0;
@@ -364,13 +365,13 @@ __device__ void item_A(const StepParams& P, int b, int idx, const ItemRef& nxt, 
             float cm = -FLT_MAX;
 #pragma unroll
             for (int j = 0; j < kAVec; ++j) AStat<T>::minmax(w[j], cm, mn);
-            // The thread's max grew: rescale its running sum (fp64).  A warp vote
-            // keeps this a real (rarely taken) branch instead of predicated code.
-            if (__any_sync(kFull, cm > m)) {
-                if (cm > m) {
-                    if (s != 0.0) s *= exp((double)m - (double)cm);
-                    m = cm;
-                }
+            // Warp-uniform running max: when the warp's max grows (rarely, after
+            // the first chunks) every lane rescales its fp64 sum by the same
+            // factor, and the end-of-run fold needs no exp at all.
+            cm = warp_max(cm);
+            if (cm > m) {
+                if (s != 0.0) s *= exp((double)m - (double)cm);
+                m = cm;
             }
             if (m != -FLT_MAX) {  // a thread that has seen pads only contributes nothing
                 const float2 negM = make_float2(-m, -m);
@@ -380,7 +381,8 @@ __device__ void item_A(const StepParams& P, int b, int idx, const ItemRef& nxt, 
                     if (j & 1) AStat<T>::expsum(w[j], negM, s1);
                     else AStat<T>::expsum(w[j], negM, s0);
                 }
-                s += ((double)s0.x + (double)s0.y) + ((double)s1.x + (double)s1.y);
+                const float2 t = __fadd2_rn(s0, s1);  // <= 16 fp32 terms per pair lane, then fp64
+                s += (double)t.x + (double)t.y;
             }
         }
     }
@@ -389,9 +391,14 @@ __device__ void item_A(const StepParams& P, int b, int idx, const ItemRef& nxt, 
     if (__any_sync(kFull, isinf(mn)) && lane == 0) flag(P, SSV_STATUS_NONFINITE);
     // Warp fold (fixed order, fp64) -> one partial per warp; no CTA barrier, so
     // the warps of a CTA drift freely between runs.
-    const double md = (double)m;
-    double M = warp_max(md);
-    const double S = warp_sum(s != 0.0 ? s * exp(md - M) : s);  // NaN propagates
+    double M = (double)m;  // warp-uniform (fp32 path); fp64 storage keeps per-lane maxima
+    double S;
+    if constexpr (sizeof(T) == 8) {
+        M = warp_max((double)m);
+        S = warp_sum(s != 0.0 ? s * exp((double)m - M) : s);  // NaN propagates
+    } else {
+        S = warp_sum(s);
+    }
     if (lane == 0) {
         if (isnan(S) || M == CUDART_INF) flag(P, SSV_STATUS_NONFINITE);
         if (S == 0.0) M = -CUDART_INF;  // a warp that saw pads only
@@ -1446,6 +1453,8 @@ void plan_geometry(int dtype, int act, StepParams& P) {
         }();
         long want = ((long)P.Kc * P.B * P.NR + 4 * resident - 1) / (4 * resident);
         want = std::max<long>(1, std::min<long>({want, (long)P.Kc, (long)run_cap}));
+        static const int run_force = getenv("SSV_RUNA_FORCE") ? atoi(getenv("SSV_RUNA_FORCE")) : 0;  // experiment knob
+        if (run_force > 0) want = std::min<long>(run_force, P.Kc);
         const long runs = (P.Kc + want - 1) / want;
         P.runA = (int)((P.Kc + runs - 1) / runs);
         P.K = (P.Kc + P.runA - 1) / P.runA;
@@ -1535,6 +1544,8 @@ static void launch_verify_t(const StepParams& P, const Launch& L) {
     const unsigned grid = std::min<unsigned>(P.n_items, (unsigned)(sm_count() * per_sm));
     StepParams Q = P;
     Q.claim_ahead = P.n_items > 2u * grid;
+    static const int dbgm = getenv("SSV_DBG_MODE") ? atoi(getenv("SSV_DBG_MODE")) : 0;
+    Q.dbg = dbgm;
     const int h = L.begin(KID_VERIFY);
     k_verify<T, ACT><<<grid, kCtaThreads, kDynSmem, L.st>>>(Q);
     L.end(h);
