@@ -45,6 +45,7 @@ WORKLOADS = {
     "c3bf16": ("C3 Llama-2-shape verify B=64 gamma=8 V=32000 bf16", 64, 8, 32000, "bf16"),
     "c4": ("C4 large-vocab verify B=256 gamma=8 V=151936 fp32 (per GPU)", 256, 8, 151936, "f32"),
     "c4shard": ("C4 large-vocab verify B=32/GPU (256 over 8 GPUs) gamma=8 V=151936 fp32", 32, 8, 151936, "f32"),
+    "c4bf16": ("C4 large-vocab verify B=256 gamma=8 V=151936 bf16 (per GPU)", 256, 8, 151936, "bf16"),
 }
 BYTES = {"f32": 4, "bf16": 2, "f64": 8}
 
@@ -475,8 +476,10 @@ def main():
             line["cpu_baseline"] = {"value": None, "error": str(e)}
     if rank == 0 and world == 1 and not args.no_extra:
         extra = {}
-        for key, variant in (("c2", "sigmoid" if args.variant == "exact" else "exact"), ("c3", "exact"),
-                             ("c3bf16", "exact"), ("c3", "sigmoid"), ("c4", "exact"), ("c4", "sigmoid")):
+        for key, variant in (("c2", "sigmoid" if args.variant == "exact" else "exact"), ("c1", "exact"),
+                             ("c1", "sigmoid"), ("c3", "exact"), ("c3bf16", "exact"), ("c3", "sigmoid"),
+                             ("c3bf16", "sigmoid"), ("c4", "exact"), ("c4", "sigmoid"), ("c4bf16", "exact"),
+                             ("c4shard", "exact")):
             if key == args.workload and variant == args.variant:
                 continue
             try:

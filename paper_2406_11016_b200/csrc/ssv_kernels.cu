@@ -701,7 +701,7 @@ __device__ __forceinline__ double2 granule_reduce(const StepParams& P, const Dec
 #pragma unroll
         for (int t = 0; t < EPL; ++t) {
             if (t * 32 + lane < n) {
-                if (ACT == ACT_SIGMOID) sm += (A)1 / ((A)1 + exp_neg((D.xs[t] - alpha) * invw));
+                if (ACT == ACT_SIGMOID) sm += sigmoid_fast((D.xs[t] - alpha) * invw);
                 else sm += D.xs[t];
             }
         }
@@ -722,8 +722,8 @@ __device__ __forceinline__ double2 granule_reduce(const StepParams& P, const Dec
                 // sigma(tp) - sigma(tq) = sigma(tp) sigma(-tq) (1 - e^-(tp-tq)): no cancellation.
                 const A tp_ = (xp - alpha) * invw, tq_ = (xqq - alpha) * invw;
                 const A dd = (xp - xqq) * invw;
-                vp = (A)1 / ((A)1 + exp_neg(tp_));
-                const A sqn = (A)1 / ((A)1 + exp_neg(-tq_));
+                vp = sigmoid_fast(tp_);
+                const A sqn = sigmoid_fast(-tq_);
                 a = dd > (A)0 ? vp * sqn * (-expm1_acc(-dd)) : (A)0;
             } else {
                 vp = xp;
@@ -1316,7 +1316,7 @@ __global__ void __launch_bounds__(kThreads) k_materialize(StepParams P, void* ou
     const A alpha = (A)P.alpha, invw = (A)(1.0 / P.width);
     auto act = [&](A x, const double2& st) -> A {
         if (ACT == ACT_SOFTMAX) return exp_rel(x, (A)st.x) * (A)(1.0 / st.y);
-        if (ACT == ACT_SIGMOID) return (A)1 / ((A)1 + exp_neg((x - alpha) * invw));
+        if (ACT == ACT_SIGMOID) return sigmoid_fast((x - alpha) * invw);
         return x;
     };
     auto stat_of = [&](int b, int r) -> double2 {
