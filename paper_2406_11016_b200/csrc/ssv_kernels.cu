@@ -198,17 +198,23 @@ struct AStat<float> {
 
 template <>
 struct AStat<__nv_bfloat16> {
+    // max / min are exact in bf16: reduce the 8 packed values with VHMNMX.BF16_V2
+    // (two per instruction, three inputs) and widen only the two survivors.
+    static __device__ __forceinline__ uint32_t max2(uint32_t a, uint32_t b) {
+        uint32_t r;
+        asm("max.bf16x2 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
+        return r;
+    }
+    static __device__ __forceinline__ uint32_t min2(uint32_t a, uint32_t b) {
+        uint32_t r;
+        asm("min.bf16x2 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
+        return r;
+    }
     static __device__ __forceinline__ void minmax(const uint4& v, float& m, float& n) {
-        float x[8];
-        unpack(v, x);
-        m = fmax3f(m, x[0], x[1]);
-        m = fmax3f(m, x[2], x[3]);
-        m = fmax3f(m, x[4], x[5]);
-        m = fmax3f(m, x[6], x[7]);
-        n = fmin3f(n, x[0], x[1]);
-        n = fmin3f(n, x[2], x[3]);
-        n = fmin3f(n, x[4], x[5]);
-        n = fmin3f(n, x[6], x[7]);
+        const uint32_t mx = max2(max2(v.x, v.y), max2(v.z, v.w));
+        const uint32_t mi = min2(min2(v.x, v.y), min2(v.z, v.w));
+        m = fmax3f(m, __uint_as_float(mx << 16), __uint_as_float(mx & 0xffff0000u));
+        n = fmin3f(n, __uint_as_float(mi << 16), __uint_as_float(mi & 0xffff0000u));
     }
     static __device__ __forceinline__ void expsum(const uint4& v, float2 negM, float2& s) {
         const float2 l2e = make_float2(1.4426950408889634f, 1.4426950408889634f);
@@ -662,8 +668,40 @@ __device__ __forceinline__ void granule_load(const StepParams& P, int b, int g, 
     const bool reject = d.mode == MODE_REJECT;
     const T* pr = p_row<T>(P, b, d.row) + lo;
     const T* qr = reject ? q_row<T>(P, b, d.row) + lo : pr;
+    constexpr int EPL = GranuleData<T>::EPL;
+    if constexpr (sizeof(T) == 2) {
+        // bf16, full granule of 16-byte-aligned rows: each lane takes 16
+        // consecutive elements with two 128-bit loads (the sums only need the
+        // granule's set).  (fp32 keeps the coalesced scalar loads: with two
+        // granules in flight the vector temporaries spill at 80 registers.)
+        constexpr int NV = EPL * (int)sizeof(T) / 16;  // vectors per lane per row (4 fp32, 2 bf16)
+        const bool vec = D.n == kGW && ((reinterpret_cast<uintptr_t>(pr) | reinterpret_cast<uintptr_t>(qr)) & 15) == 0;
+        if (vec) {
+            const uint4* vp = reinterpret_cast<const uint4*>(pr) + lane * NV;
+            const uint4* vq = reinterpret_cast<const uint4*>(qr) + lane * NV;
+            uint4 wp[NV], wq[NV];
 #pragma unroll
-    for (int t = 0; t < GranuleData<T>::EPL; ++t) {
+            for (int k = 0; k < NV; ++k) {
+                wp[k] = __ldg(vp + k);
+                if (reject) wq[k] = __ldg(vq + k);
+            }
+            constexpr int VEC = Elem<T>::VEC;
+#pragma unroll
+            for (int k = 0; k < NV; ++k) {
+                A xp[VEC], xq[VEC];
+                unpack(wp[k], xp);
+                if (reject) unpack(wq[k], xq);
+#pragma unroll
+                for (int e = 0; e < VEC; ++e) {
+                    D.xs[k * VEC + e] = xp[e];
+                    D.xq[k * VEC + e] = reject ? xq[e] : (A)0;
+                }
+            }
+            return;
+        }
+    }
+#pragma unroll
+    for (int t = 0; t < EPL; ++t) {
         const int e = t * 32 + lane;
         D.xs[t] = e < D.n ? load_elem(pr + e) : (A)0;
         D.xq[t] = (reject && e < D.n) ? load_elem(qr + e) : (A)0;

@@ -7,6 +7,8 @@ run() { # name env...
   python -c "
 import json;d=json.load(open('$OUT/exp_$name.json'));print('$name', round(d['ms_per_step']*1e3,1),'us/step', round(d['roofline']['kernel_ms']*1e3,1),'us kernel', round(d['roofline']['frac'],3))" >> $OUT/exp_summary.txt 2>&1
 }
-for r in 1 2 4; do WL=c3 run c3_aonly_r$r SSV_AONLY=1 SSV_RUNA_FORCE=$r; done
-WL=c3 run c3_full X=1
-ST=30 WL=c4 run c4_full X=1
+ST=30 WL=c4bf16 run c4bf16 X=1
+ST=30 WL=c4 run c4 X=1
+WL=c3 run c3 X=1
+ST=30 WL=c4 VAR=sigmoid run c4sig X=1
+ST=30 WL=c4bf16 VAR=sigmoid run c4bf16sig X=1
