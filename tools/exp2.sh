@@ -1,6 +1,4 @@
 set -u
 OUT=gpurun_out
 timeout 300 python tools/dbg_probs.py > $OUT/dbg.txt 2>&1
-for tool in memcheck racecheck synccheck; do
-timeout 900 /usr/local/cuda/bin/compute-sanitizer --tool $tool python tools/dbg_probs.py > $OUT/san_$tool.txt 2>&1
-done
+timeout 600 python -m pytest tests -m gpu -x -q --timeout 120 > $OUT/pytest_gpu.txt 2>&1; echo "pytest rc=$?" >> $OUT/pytest_gpu.txt
