@@ -64,6 +64,8 @@ struct Shared {
     double2 wpart[kWarps];
     double2 gpart2[kWarps * kBG];
     double2 rs[kMaxRowsSmem];
+    double loc_d[4];  // locate: carry, denominator, bonus-row max / sum
+    int loc_g, loc_useA;
 };
 
 // ---------------------------------------------------------------------------
@@ -787,101 +789,129 @@ __device__ void granule(const StepParams& P, int b, int g, const Decision& d, do
 // granule prefix (contiguous ownership, one scan) -> exact fp64 scan inside
 // the selected granule (dist.cpp:122-137, incl. both fallbacks).
 template <typename T, int ACT>
-__device__ void locate(const StepParams& P, int b, const Decision& d, Shared& sh, double2* gcache,
+__device__ void locate(const StepParams& P, int b, const Decision& d, Shared& sh, double2* gcache, double u,
                        bool cached = false) {
     const int NG = P.NG, GW = kGW;
     const double2* gp = P.gpart + (size_t)b * NG;  // (cached: gcache already holds all NG <= kLocCap)
     const T* pr = p_row<T>(P, b, d.row);
     const T* qr = d.mode == MODE_REJECT ? q_row<T>(P, b, d.row) : nullptr;
-    const double u = __ldcg(&P.u[(size_t)b * (P.G + 1) + P.G]);  // u_final, verify_reference.cpp:98
+    // u = u_final (verify_reference.cpp:98), loaded by the caller ahead of time
+    if (P.trace && b == 0 && threadIdx.x == 0) trace(P, 8 * P.B + 21);
     const int ncache = min(NG, kLocCap);
     if (!cached)
         for (int g = threadIdx.x; g < ncache; g += kCtaThreads) gcache[g] = __ldcg(&gp[g]);
     __syncthreads();
     auto raw = [&](int g) -> double2 { return g < kLocCap ? gcache[g] : __ldcg(&gp[g]); };
 
+    // Level 1 on warp 0 alone (no block barriers): the denominators, then the
+    // fp64 granule prefix over contiguous lane ranges (verify_reference.cpp:
+    // 51-62 / dist.cpp:122-137 at granule resolution); lane 0 publishes.
+    if (threadIdx.x < 32) {
+        const int lane = threadIdx.x;
+        const int gpl = (NG + 31) / 32;
+        const int ga = min(NG, lane * gpl), gb = min(NG, ga + gpl);
+        bool useA = false;
+        double denom = 1.0, gM = 0.0, gS = 1.0;
+        if (d.mode == MODE_REJECT) {
+            double a1 = 0.0, a2 = 0.0;
+            for (int g = ga; g < gb; ++g) {
+                const double2 v = raw(g);
+                a1 += v.x;
+                a2 += v.y;
+            }
+            const double sa = warp_sum(a1), sp = warp_sum(a2);
+            useA = sa > kZeroEps;  // verify_reference.cpp:57-62
+            denom = useA ? sa : sp;
+            if (lane == 0) {
+                if (P.rsu) P.rsu[b] = 1;
+                if (P.rden) P.rden[b] = useA ? sa : 0.0;
+            }
+        } else {
+            if (ACT == ACT_SOFTMAX) {  // the bonus row's statistics from its granules
+                double m = -CUDART_INF;
+                for (int g = ga; g < gb; ++g) m = fmax(m, raw(g).x);
+                gM = warp_max(m);
+                double sm = 0.0;
+                for (int g = ga; g < gb; ++g) {
+                    const double2 v = raw(g);
+                    const double w = v.y > 0.0 ? v.y * exp(v.x - gM) : 0.0;
+                    sm += w;
+                    // rebase the cached granule to the row max: (gM, w) is the same
+                    // mass, and the scans below need no further exp
+                    if (g < kLocCap) gcache[g] = make_double2(gM, w);
+                }
+                gS = warp_sum(sm);
+            } else {
+                double sm = 0.0;
+                for (int g = ga; g < gb; ++g) sm += raw(g).y;
+                denom = warp_sum(sm);
+            }
+            if (lane == 0) {
+                if (P.rsu) P.rsu[b] = 0;
+                if (P.rden) P.rden[b] = 0.0;
+            }
+        }
+        // Granule masses at granule resolution only pick the granule (the exact
+        // per-term division happens in level 2): a reciprocal is enough here.
+        const double inv = 1.0 / (d.mode != MODE_REJECT && ACT == ACT_SOFTMAX ? gS : denom);
+        auto mass = [&](int g) -> double {
+            const double2 v = raw(g);
+            if (d.mode == MODE_REJECT) return (useA ? v.x : v.y) * inv;
+            if (ACT == ACT_SOFTMAX) return v.y > 0.0 ? (g < kLocCap ? v.y : v.y * exp(v.x - gM)) * inv : 0.0;
+            return v.y * inv;
+        };
+        double tsum = 0.0;
+        for (int g = ga; g < gb; ++g) tsum += mass(g);
+        double run = warp_scan_incl(tsum) - tsum;
+        int hit = 0x7fffffff;
+        double hit_carry = 0.0;
+        for (int g = ga; g < gb; ++g) {
+            const double w = mass(g);
+            if (u < run + w) {
+                hit = g;
+                hit_carry = run;
+                break;
+            }
+            run += w;
+        }
+        const unsigned hm = __ballot_sync(kFull, hit != 0x7fffffff);
+        const int src = hm ? __ffs(hm) - 1 : 0;
+        const int gst = __shfl_sync(kFull, hit, src);
+        const double car = __shfl_sync(kFull, hit_carry, src);
+        if (lane == 0) {
+            sh.loc_g = hm ? gst : -1;
+            sh.loc_useA = useA;
+            sh.loc_d[0] = car;
+            sh.loc_d[1] = denom;
+            sh.loc_d[2] = gM;
+            sh.loc_d[3] = gS;
+        }
+    }
+    __syncthreads();
     RowCtx R;
     R.mode = d.mode;
     R.Mp = d.Mp;
     R.Sp = d.Sp;
     R.Mq = d.Mq;
     R.Sq = d.Sq;
-    R.useA = false;
-    R.denom = 1.0;
-    double gM = 0.0, gS = 1.0;
-    if (d.mode == MODE_REJECT) {
-        double sa = 0.0, sp = 0.0;
-        for (int g = threadIdx.x; g < NG; g += kCtaThreads) {
-            const double2 v = raw(g);
-            sa += v.x;
-            sp += v.y;
-        }
-        sa = block_reduce(sa, sh.dred, OpSum());
-        sp = block_reduce(sp, sh.dred, OpSum());
-        R.useA = sa > kZeroEps;  // verify_reference.cpp:57-62
-        R.denom = R.useA ? sa : sp;
-        if (threadIdx.x == 0) {
-            if (P.rsu) P.rsu[b] = 1;
-            if (P.rden) P.rden[b] = R.useA ? sa : 0.0;
-        }
-    } else {
-        if (ACT == ACT_SOFTMAX) {  // the bonus row's statistics from its granules
-            double m = -CUDART_INF;
-            for (int g = threadIdx.x; g < NG; g += kCtaThreads) m = fmax(m, raw(g).x);
-            gM = block_reduce(m, sh.dred, OpMax());
-            double sm = 0.0;
-            for (int g = threadIdx.x; g < NG; g += kCtaThreads) {
-                const double2 v = raw(g);
-                if (v.y > 0.0) sm += v.y * exp(v.x - gM);
-            }
-            gS = block_reduce(sm, sh.dred, OpSum());
-            R.Mp = gM;
-            R.Sp = gS;
-            R.denom = 1.0;  // sample_row's sequential_sum of a softmax row (1 within rounding)
-        } else {
-            double sm = 0.0;
-            for (int g = threadIdx.x; g < NG; g += kCtaThreads) sm += raw(g).y;
-            R.denom = block_reduce(sm, sh.dred, OpSum());
-        }
-        if (threadIdx.x == 0) {
-            if (P.rsu) P.rsu[b] = 0;
-            if (P.rden) P.rden[b] = 0.0;
-        }
+    R.useA = sh.loc_useA;
+    R.denom = sh.loc_d[1];
+    const double gM = sh.loc_d[2], gS = sh.loc_d[3];
+    if (d.mode != MODE_REJECT && ACT == ACT_SOFTMAX) {
+        R.Mp = gM;
+        R.Sp = gS;
+        R.denom = 1.0;  // sample_row's sequential_sum of a softmax row (1 within rounding)
     }
-    auto gmass = [&](int g) -> double {  // normalized granule mass
+    auto gmass = [&](int g) -> double {  // normalized granule mass (fallback path)
         const double2 v = raw(g);
         if (R.mode == MODE_REJECT) return (R.useA ? v.x : v.y) / R.denom;
         if (ACT == ACT_SOFTMAX) return v.y > 0.0 ? v.y * exp(v.x - gM) / gS : 0.0;
         return v.y / R.denom;
     };
-
-    // Level 1: contiguous granule ownership, one block scan.
-    const int gpt = (NG + kCtaThreads - 1) / kCtaThreads;
-    const int ga = min(NG, (int)threadIdx.x * gpt), gb = min(NG, ga + gpt);
-    double tsum = 0.0;
-    for (int g = ga; g < gb; ++g) tsum += gmass(g);
-    double total;
-    double run = block_scan_incl(tsum, sh.dred, total) - tsum;
-    int hit = 0x7fffffff;
-    double hit_carry = 0.0;
-    for (int g = ga; g < gb; ++g) {
-        const double w = gmass(g);
-        if (u < run + w) {
-            hit = g;
-            hit_carry = run;
-            break;
-        }
-        run += w;
-    }
-    int gstar = block_reduce(hit, sh.ired, OpMin());
-    double carry = 0.0;
-    if (gstar != 0x7fffffff) {
-        if (hit == gstar) sh.dred[0] = hit_carry;  // block_reduce's barriers ordered every earlier dred read
-        __syncthreads();
-        carry = sh.dred[0];
-    } else {
-        gstar = -1;
-    }
+    int gstar = sh.loc_g;
+    double carry = sh.loc_d[0];
+    const bool tl = P.trace && b == 0 && threadIdx.x == 0;  // locate stamps: trace[8B + 18 ..]
+    if (tl) trace(P, 8 * P.B + 18);
 
     // Level 2: exact element scan, continuing into later granules on rounding.
     int token = -1;
@@ -895,8 +925,8 @@ __device__ void locate(const StepParams& P, int b, const Decision& d, Shared& sh
         if (base < hi) v0 = exact_value<T, ACT>(P, R, pr, qr, base) / R.denom;
         if (base + 1 < hi) v1 = exact_value<T, ACT>(P, R, pr, qr, base + 1) / R.denom;
         const double ts = v0 + v1;
+        if (tl) trace(P, 8 * P.B + 19);
         double tot;
-        __syncthreads();  // sh.dred[0] (carry) has been read by every thread
         const double incl = block_scan_incl(ts, sh.dred, tot);
         double cum = carry + (incl - ts);
         int h = 0x7fffffff;
@@ -927,6 +957,7 @@ __device__ void locate(const StepParams& P, int b, const Decision& d, Shared& sh
             if (last >= 0) token = last;
         }
     }
+    if (tl) trace(P, 8 * P.B + 20);
     if (threadIdx.x == 0) P.fin[b] = token;
 }
 
@@ -1013,6 +1044,7 @@ template <typename T, int ACT>
 __device__ void item_L(const StepParams& P, int b, Shared& sh, double2* gcache) {
     const int tid = threadIdx.x;
     if (tid == 0) trace(P, 8 * b + 5);
+    const double u = __ldcg(&P.u[(size_t)b * (P.G + 1) + P.G]);  // u_final, issued before the waits
     get_decision<T, ACT>(P, b, true, sh);
     const Decision d = sh.dec;
     if (tid == 0) {
@@ -1021,7 +1053,7 @@ __device__ void item_L(const StepParams& P, int b, Shared& sh, double2* gcache) 
     }
     __syncthreads();
     if (d.mode != MODE_NONE) {
-        locate<T, ACT>(P, b, d, sh, gcache);
+        locate<T, ACT>(P, b, d, sh, gcache, u);
         if (tid == 0) trace(P, 8 * b + 7);
     }
     if (tid == 0) {  // every B-item of b has read the flag and been counted
@@ -1335,7 +1367,7 @@ __global__ void __launch_bounds__(kCtaThreads, 1) k_verify_cluster(StepParams P)
     cl.sync();  // rank 0 is done reading the others' shared memory
     if (rank != 0) return;
     if (tr) trace(P, 8 * b + 6);
-    locate<T, ACT>(P, b, d, sh, gcache, /*cached=*/true);
+    locate<T, ACT>(P, b, d, sh, gcache, zg[2 * G + G], /*cached=*/true);
     if (tr) {
         trace(P, 8 * b + 7);
         atomicMax(&P.trace[8 * P.B + 1], gtime());
@@ -1563,7 +1595,7 @@ void plan_geometry(int dtype, int act, StepParams& P) {
     P.n_items = item;
 }
 
-int trace_slots(const StepParams& P) { return 8 * P.B + 18; }
+int trace_slots(const StepParams& P) { return 8 * P.B + 26; }
 
 template <typename T, int ACT>
 static void launch_verify_t(const StepParams& P, const Launch& L) {

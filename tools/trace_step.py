@@ -23,7 +23,7 @@ run = (lambda: v.verify_exact(zp, zq, ids, u)) if a.variant == "exact" else (lam
 for _ in range(3):
     run()
 torch.cuda.synchronize()
-cap = 8 * a.B + 18
+cap = 8 * a.B + 26
 v.trace_enable(cap)
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 s = torch.cuda.Stream()
@@ -48,3 +48,7 @@ for b in rows:
 ex = t[8 * a.B + 2: 8 * a.B + 18]
 if ex[0] > 0:
     print("row-0 fine stamps (us):", " ".join(f"{(x - t0) / 1e3:.1f}" if x > 0 else "-" for x in ex))
+lo = t[8 * a.B + 18: 8 * a.B + 22]
+if lo[3] > 0:
+    f2 = lambda x: f"{(x - t0) / 1e3:.1f}" if x > 0 else "-"
+    print(f"row-0 locate (us): enter {f2(lo[3])} level1-done {f2(lo[0])} level2-values {f2(lo[1])} end {f2(lo[2])}")
