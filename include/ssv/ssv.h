@@ -93,6 +93,15 @@ void* ssv_get_stream(const ssv_ctx* ctx);
 const char* ssv_last_error(const ssv_ctx* ctx);
 /* Number of kernels the last verify/sample/generate call launched. */
 int ssv_last_launch_count(const ssv_ctx* ctx);
+
+/* Kernel selection for the verify entry points: AUTO
+ * picks the cluster kernel when every batch row can get a resident thread-
+ * block cluster, else the streaming kernel.  Both give identical results up to
+ * the summation order of the fp32 partial sums (same parity bar). */
+#define SSV_PATH_AUTO 0
+#define SSV_PATH_STREAMING 1
+#define SSV_PATH_CLUSTER 2 /* falls back to streaming where the cluster kernel cannot run */
+int ssv_set_path(ssv_ctx* ctx, int32_t path);
 const char* ssv_version(void);
 
 /* Kernel timing.  While enabled, each kernel launch of this context (up to
@@ -108,10 +117,11 @@ int ssv_profile_reset(ssv_ctx* ctx);
 int ssv_profile_read(ssv_ctx* ctx, int32_t kernel_id, double* total_ms, int32_t* count);
 
 /* Diagnostics.  capacity > 0 with host_out == NULL attaches a device buffer
- * of `capacity` globaltimer stamps (ns) that verify launches fill: [2 * grid]
- * per-CTA start/end, then [4 * B] per batch row decide start/end and locate
- * start/end.  host_out != NULL copies the buffer out (after a stream sync);
- * capacity 0 detaches it. */
+ * of `capacity` globaltimer stamps (ns) that verify launches fill when it holds
+ * at least 8 * B + 26 slots: [8 * B] per-batch-row phase stamps, then kernel
+ * start / end and finer stamps of batch row 0 (layout: tools/trace_step.py).
+ * host_out != NULL copies the buffer out (after a stream sync); capacity 0
+ * detaches it. */
 int ssv_debug_trace(ssv_ctx* ctx, int capacity, unsigned long long* host_out, int* grid_out);
 
 /* ---- stream-ordered entry points: every pointer is DEVICE memory ----------- */

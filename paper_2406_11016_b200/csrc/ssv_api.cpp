@@ -34,6 +34,7 @@ struct ssv_ctx {
     uint32_t* status_host = nullptr;  // pinned
     ProfileHook prof;
     bool profiling = false;
+    int path = SSV_PATH_AUTO;
     unsigned long long* trace = nullptr;  // diagnostics (ssv_debug_trace)
     int trace_cap = 0;
     Launch launcher() { return Launch{stream, &launches, profiling ? &prof : nullptr}; }
@@ -178,7 +179,7 @@ int run_device(ssv_ctx* ctx, int variant, const ssv_verify_args* a, ssv_verify_o
     P.width = a->beta - a->alpha;
     P.check_uniforms = variant != V_SIGMOID;
     plan_geometry(a->dtype, variant, P);
-    plan_cluster(a->dtype, variant, P);
+    if (ctx->path != SSV_PATH_STREAMING) plan_cluster(a->dtype, variant, P);
     const Layout L = plan_scratch(P, 0);
     rc = ensure_scratch(ctx, L.total, (size_t)P.B);
     if (rc) return rc;
@@ -358,6 +359,14 @@ void* ssv_get_stream(const ssv_ctx* ctx) { return ctx ? static_cast<void*>(ctx->
 const char* ssv_last_error(const ssv_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
 
 int ssv_last_launch_count(const ssv_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+int ssv_set_path(ssv_ctx* ctx, int32_t path) {
+    if (!ctx) return SSV_EINVAL;
+    if (path != SSV_PATH_AUTO && path != SSV_PATH_STREAMING && path != SSV_PATH_CLUSTER)
+        return fail(ctx, SSV_EINVAL, "ssv_set_path: unknown path %d", path);
+    ctx->path = path;
+    return SSV_OK;
+}
 
 int ssv_profile_enable(ssv_ctx* ctx, int capacity) {
     if (!ctx || capacity < 1) return SSV_EINVAL;

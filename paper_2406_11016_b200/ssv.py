@@ -88,6 +88,7 @@ def load_library() -> C.CDLL:
         L.ssv_last_error.argtypes = [vp]
         L.ssv_last_error.restype = C.c_char_p
         L.ssv_last_launch_count.argtypes = [vp]
+        L.ssv_set_path.argtypes = [vp, i32]
         for name in ("exact", "sigmoid", "probs", "exact_host", "sigmoid_host", "probs_host"):
             f = getattr(L, "ssv_verify_" + name)
             f.argtypes = [vp, C.POINTER(Args), C.POINTER(Out)]
@@ -113,7 +114,7 @@ EXPORTS = (
     "ssv_verify_probs", "ssv_verify_exact_host", "ssv_verify_sigmoid_host", "ssv_verify_probs_host",
     "ssv_host_alloc", "ssv_host_free", "ssv_sample_softmax", "ssv_make_bench_inputs",
     "ssv_profile_enable", "ssv_profile_disable", "ssv_profile_reset", "ssv_profile_read",
-    "ssv_debug_trace",
+    "ssv_debug_trace", "ssv_set_path",
 )
 
 KID_VERIFY, KID_MATERIALIZE, KID_GEN = 0, 2, 3
@@ -198,6 +199,11 @@ class Verifier:
             import torch
 
             self.lib.ssv_set_stream(self.ctx, C.c_void_p(torch.cuda.current_stream(self.device).cuda_stream))
+
+    def set_path(self, path: str) -> None:
+        """Kernel selection: "auto" (default), "streaming" or "cluster" (ssv_set_path)."""
+        code = {"auto": 0, "streaming": 1, "cluster": 2}[path]
+        self._check(self.lib.ssv_set_path(self.ctx, code), "ssv_set_path")
 
     @property
     def stream_handle(self) -> int:

@@ -311,3 +311,47 @@ def test_full_size_c4_row_subsample(verifier, oracle):
     assert ((r.final_token >= 0) & (r.final_token < V)).all()
     assert (r.resample_used == (r.accepted_len < gamma)).all()
     assert ((r.tau >= 0) & (r.tau <= 1)).all()
+
+
+@pytest.mark.parametrize("path", ["streaming", "cluster"])
+def test_both_kernels_small_shapes(verifier, oracle, path):
+    """The streaming and the cluster kernel each on the small shapes the auto
+    choice would route to the other one (validate.cpp:221-321-style grid)."""
+    rng = np.random.default_rng({"streaming": 11, "cluster": 12}[path])
+    state = (0x5EED + len(path), 0)
+    verifier.set_path(path)
+    try:
+        mism = 0
+        for i in range(24):
+            B = int(rng.choice([1, 3, 8]))
+            gamma = int(rng.integers(1, 12))
+            V = int(rng.choice([7, 257, 4099, 51865, 32000]))
+            bonus = bool(rng.integers(0, 2))
+            (zp, zq, ids, u), state = oracle.make_logit_instance(state, B, gamma, V, bonus, 3.0)
+            zp, zq = oracle.round_f32(zp), oracle.round_f32(zq)
+            o = oracle.verify_exact(zp, zq, ids, u)
+            g = _run(verifier, "exact", *to_device(oracle, zp, zq, ids, u, "f32"))
+            mism += compare(o, g, zp, zq, ids, u, "exact", label=f"{path}-exact{i}")
+            o = oracle.verify_sigmoid(zp, zq, ids, u, -1e3, 1e3)
+            g = _run(verifier, "sigmoid", *to_device(oracle, zp, zq, ids, u, "f32"))
+            mism += compare(o, g, zp, zq, ids, u, "sigmoid", label=f"{path}-sig{i}")
+        assert mism <= 1
+    finally:
+        verifier.set_path("auto")
+
+
+def test_streaming_and_cluster_agree_on_c2(verifier, oracle):
+    """C2 (the headline shape) through both kernels: identical decisions and
+    tokens, tau / denominators within the parity tolerance (the two kernels sum
+    the fp32 chunk partials in different orders: ~1e-7 relative apart)."""
+    zp, zq, ids, u = oracle.make_bench_batch(1, 8, 5, 51865)
+    zp, zq = oracle.round_f32(zp), oracle.round_f32(zq)
+    t = to_device(oracle, zp, zq, ids, u, "f32")
+    res = {}
+    for path in ("streaming", "cluster"):
+        verifier.set_path(path)
+        res[path] = _run(verifier, "exact", *t).numpy()
+    verifier.set_path("auto")
+    a, b = res["streaming"], res["cluster"]
+    assert np.array_equal(a.accepted_len, b.accepted_len) and np.array_equal(a.final_token, b.final_token)
+    assert np.abs(a.tau - b.tau).max() < 1e-6 and np.abs(a.residual_denom - b.residual_denom).max() < 1e-6
