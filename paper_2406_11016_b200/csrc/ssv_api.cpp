@@ -19,6 +19,8 @@ using namespace ssv;
 struct ssv_ctx {
     int device = 0;
     cudaStream_t own = nullptr;
+    cudaStream_t aux = nullptr;           // host entry points: second copy stream (second copy engine)
+    cudaEvent_t fork = nullptr, join = nullptr;
     cudaStream_t stream = nullptr;
     std::string err;
     int launches = 0;
@@ -32,6 +34,8 @@ struct ssv_ctx {
     void* stage = nullptr;
     size_t stage_bytes = 0;
     uint32_t* status_host = nullptr;  // pinned
+    void* hstage = nullptr;           // pinned mirror of the small host-entry inputs / outputs
+    size_t hstage_bytes = 0;
     ProfileHook prof;
     bool profiling = false;
     int path = SSV_PATH_AUTO;
@@ -242,15 +246,21 @@ int run_host(ssv_ctx* ctx, int variant, const ssv_verify_args* a, ssv_verify_out
     struct Piece {
         size_t off, bytes;
     };
+    // Device staging: the logits, then ONE block of small inputs (ids, uniforms,
+    // a zeroed status word) and ONE block of small outputs, so a call costs two
+    // big copies + one small H2D + one small D2H (each API call is microseconds).
     size_t off = 0;
     auto take = [&](size_t bytes) {
         Piece p{off, bytes};
         off = align_up(off + bytes);
         return p;
     };
-    const Piece zp = take(np * es), zq = take(nq * es), ids = take(B * G * 4), u = take(B * (G + 1) * 8);
-    const Piece acc = take(B * 4), fin = take(B * 4), rsu = take(B), tau = take(B * G * 8), rden = take(B * 8),
-                st = take(4);
+    const Piece zp = take(np * es), zq = take(nq * es);
+    const size_t small0 = off;
+    const Piece ids = take(B * G * 4), u = take(B * (G + 1) * 8), st = take(4);
+    const size_t small_in = off - small0;
+    const Piece acc = take(B * 4), fin = take(B * 4), rsu = take(B), tau = take(B * G * 8), rden = take(B * 8);
+    const size_t small_all = off - small0;
     const bool wp = a->flags & SSV_WANT_P, wq = a->flags & SSV_WANT_Q, wr = a->flags & SSV_WANT_RESIDUAL;
     const Piece pp = take(wp ? np * os : 0), pq = take(wq ? nq * os : 0), pr = take(wr ? nq * os : 0);
     if (off > ctx->stage_bytes) {
@@ -260,13 +270,33 @@ int run_host(ssv_ctx* ctx, int variant, const ssv_verify_args* a, ssv_verify_out
         CK(cudaMalloc(&ctx->stage, off));
         ctx->stage_bytes = off;
     }
+    if (small_all > ctx->hstage_bytes) {
+        CK(cudaStreamSynchronize(ctx->stream));
+        if (ctx->hstage) CK(cudaFreeHost(ctx->hstage));
+        ctx->hstage = nullptr;
+        CK(cudaMallocHost(&ctx->hstage, small_all));
+        ctx->hstage_bytes = small_all;
+    }
     char* d = static_cast<char*>(ctx->stage);
+    char* h = static_cast<char*>(ctx->hstage);  // mirrors d + small0
+    std::memcpy(h + (ids.off - small0), a->draft_tokens, ids.bytes);
+    std::memcpy(h + (u.off - small0), a->uniforms, u.bytes);
+    std::memset(h + (st.off - small0), 0, 4);
     cudaStream_t s = ctx->stream;
+    // z_q goes over a second stream so two copy engines share the link (measured
+    // on B200 / PCIe: 18 MB in 360 us on two streams vs 443 us on one).
+    if (!ctx->aux) {
+        CK(cudaStreamCreateWithFlags(&ctx->aux, cudaStreamNonBlocking));
+        CK(cudaEventCreateWithFlags(&ctx->fork, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&ctx->join, cudaEventDisableTiming));
+    }
+    CK(cudaEventRecord(ctx->fork, s));
+    CK(cudaStreamWaitEvent(ctx->aux, ctx->fork, 0));
+    CK(cudaMemcpyAsync(d + zq.off, a->z_q, zq.bytes, cudaMemcpyHostToDevice, ctx->aux));
+    CK(cudaEventRecord(ctx->join, ctx->aux));
+    CK(cudaMemcpyAsync(d + small0, h, small_in, cudaMemcpyHostToDevice, s));
     CK(cudaMemcpyAsync(d + zp.off, a->z_p, zp.bytes, cudaMemcpyHostToDevice, s));
-    CK(cudaMemcpyAsync(d + zq.off, a->z_q, zq.bytes, cudaMemcpyHostToDevice, s));
-    CK(cudaMemcpyAsync(d + ids.off, a->draft_tokens, ids.bytes, cudaMemcpyHostToDevice, s));
-    CK(cudaMemcpyAsync(d + u.off, a->uniforms, u.bytes, cudaMemcpyHostToDevice, s));
-    CK(cudaMemsetAsync(d + st.off, 0, 4, s));
+    CK(cudaStreamWaitEvent(s, ctx->join, 0));
     ssv_verify_args da = *a;
     da.z_p = d + zp.off;
     da.z_q = d + zq.off;
@@ -284,18 +314,21 @@ int run_host(ssv_ctx* ctx, int variant, const ssv_verify_args* a, ssv_verify_out
     dout.residual = wr ? d + pr.off : nullptr;
     rc = run_device(ctx, variant, &da, &dout);
     if (rc) return rc;
-    CK(cudaMemcpyAsync(o->accepted_len, dout.accepted_len, acc.bytes, cudaMemcpyDeviceToHost, s));
-    CK(cudaMemcpyAsync(o->final_token, dout.final_token, fin.bytes, cudaMemcpyDeviceToHost, s));
-    CK(cudaMemcpyAsync(o->resample_used, dout.resample_used, rsu.bytes, cudaMemcpyDeviceToHost, s));
-    CK(cudaMemcpyAsync(o->tau, dout.tau, tau.bytes, cudaMemcpyDeviceToHost, s));
-    CK(cudaMemcpyAsync(o->residual_denom, dout.residual_denom, rden.bytes, cudaMemcpyDeviceToHost, s));
-    CK(cudaMemcpyAsync(ctx->status_host, dout.status, 4, cudaMemcpyDeviceToHost, s));
+    // status word + every small output in one copy
+    CK(cudaMemcpyAsync(h + (st.off - small0), d + st.off, small_all - (st.off - small0), cudaMemcpyDeviceToHost, s));
     if (wp) CK(cudaMemcpyAsync(o->p, dout.p, pp.bytes, cudaMemcpyDeviceToHost, s));
     if (wq) CK(cudaMemcpyAsync(o->q, dout.q, pq.bytes, cudaMemcpyDeviceToHost, s));
     if (wr) CK(cudaMemcpyAsync(o->residual, dout.residual, pr.bytes, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
-    if (o->status) *o->status = *ctx->status_host;
-    return status_to_rc(ctx, *ctx->status_host);
+    std::memcpy(o->accepted_len, h + (acc.off - small0), acc.bytes);
+    std::memcpy(o->final_token, h + (fin.off - small0), fin.bytes);
+    std::memcpy(o->resample_used, h + (rsu.off - small0), rsu.bytes);
+    std::memcpy(o->tau, h + (tau.off - small0), tau.bytes);
+    std::memcpy(o->residual_denom, h + (rden.off - small0), rden.bytes);
+    uint32_t status;
+    std::memcpy(&status, h + (st.off - small0), 4);
+    if (o->status) *o->status = status;
+    return status_to_rc(ctx, status);
 }
 
 }  // namespace
@@ -343,7 +376,11 @@ void ssv_destroy(ssv_ctx* ctx) {
     if (ctx->counters) cudaFree(ctx->counters);
     if (ctx->status_dev) cudaFree(ctx->status_dev);
     if (ctx->stage) cudaFree(ctx->stage);
+    if (ctx->hstage) cudaFreeHost(ctx->hstage);
     if (ctx->status_host) cudaFreeHost(ctx->status_host);
+    if (ctx->aux) cudaStreamDestroy(ctx->aux);
+    if (ctx->fork) cudaEventDestroy(ctx->fork);
+    if (ctx->join) cudaEventDestroy(ctx->join);
     if (ctx->own) cudaStreamDestroy(ctx->own);
     delete ctx;
 }

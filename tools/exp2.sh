@@ -1,8 +1,4 @@
 set -u
 OUT=gpurun_out
-for c in "8 5 51865" "1 5 32000"; do set -- $c
-timeout 100 python tools/trace_step.py --B $1 --gamma $2 --V $3 >> $OUT/trace_cl.txt 2>&1
-done
-timeout 100 python tools/trace_step.py --B 64 --gamma 8 --V 32000 >> $OUT/trace_cl.txt 2>&1
-timeout 300 python tools/dbg_probs.py > $OUT/dbg.txt 2>&1
-timeout 600 python -m pytest tests -m gpu -x -q --timeout 120 > $OUT/pytest_gpu.txt 2>&1; echo "pytest rc=$?" >> $OUT/pytest_gpu.txt
+timeout 300 python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --master-addr 127.0.0.1 --master-port 29511 bench.py --gpus 1 --steps 50 --warmup 3 --no-extra --no-cpu --workload c4shard > $OUT/torchrun.json 2> $OUT/torchrun.err; echo "rc=$?" >> $OUT/torchrun.err
+timeout 300 python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --master-addr 127.0.0.1 --master-port 29512 bench.py --impl reference --gpus 1 --steps 3 --warmup 3 > $OUT/torchrun_ref.json 2> $OUT/torchrun_ref.err; echo "rc=$?" >> $OUT/torchrun_ref.err
