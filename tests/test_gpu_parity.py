@@ -355,3 +355,34 @@ def test_streaming_and_cluster_agree_on_c2(verifier, oracle):
     a, b = res["streaming"], res["cluster"]
     assert np.array_equal(a.accepted_len, b.accepted_len) and np.array_equal(a.final_token, b.final_token)
     assert np.abs(a.tau - b.tau).max() < 1e-6 and np.abs(a.residual_denom - b.residual_denom).max() < 1e-6
+
+
+@pytest.mark.parametrize("gamma,B,V,dtype", [
+    (1, 1024, 32000, "f32"), (16, 64, 51865, "f32"), (2, 512, 151936, "f32"), (4, 1, 151936, "f32"),
+    (16, 1, 32000, "f32"), (8, 16, 51865, "bf16"), (16, 8, 151936, "bf16"), (2, 300, 51865, "bf16"),
+])
+def test_c5_sweep_points(verifier, oracle, gamma, B, V, dtype):
+    """BASELINE config 5 sweep (gamma in 1..16, B in 1..1024, V in the three
+    vocabularies) at full size on the device, both variants: properties over
+    every row, the oracle on a row subsample (rows are independent)."""
+    import torch
+
+    tdt = {"f32": torch.float32, "bf16": torch.bfloat16}[dtype]
+    zp_t, zq_t, ids_t, u_t = verifier.make_bench_inputs(7, B, gamma, V, tdt)
+    rows = sorted({0, B // 3, B // 2, B - 1})
+    zp = zp_t[rows].double().cpu().numpy()
+    zq = zq_t[rows].double().cpu().numpy()
+    ids = ids_t[rows].cpu().numpy()
+    u = u_t[rows].cpu().numpy()
+    from paper_2406_11016_b200.ssv import VerifyResult
+
+    for kind in ("exact", "sigmoid"):
+        r = _run(verifier, kind, zp_t, zq_t, ids_t, u_t).numpy()
+        assert (r.accepted_len >= 0).all() and (r.accepted_len <= gamma).all()
+        assert ((r.final_token >= 0) & (r.final_token < V)).all()
+        assert (r.resample_used == (r.accepted_len < gamma)).all()
+        assert ((r.tau >= 0) & (r.tau <= 1)).all()
+        o = _oracle(oracle, kind, zp, zq, ids, u)
+        sub = VerifyResult(r.accepted_len[rows], r.final_token[rows], r.resample_used[rows], r.tau[rows],
+                           r.residual_denom[rows])
+        assert compare(o, sub, zp, zq, ids, u, kind, label=f"sweep-{kind}-{gamma}-{B}-{V}-{dtype}") <= 1
