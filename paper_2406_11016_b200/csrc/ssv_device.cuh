@@ -173,10 +173,10 @@ __device__ __forceinline__ V warp_min(V v) {
     return v;
 }
 
-// Block reductions over kThreads threads; `sm` needs kWarps slots.  All
-// threads receive the result.  Ends with the scratch free for reuse.
-template <typename V, typename Op>
-__device__ __forceinline__ V block_reduce(V v, V* sm, Op op) {
+// Block reductions over NW warps (default: kThreads threads); `sm` needs NW
+// slots.  All threads receive the result.  Ends with the scratch free for reuse.
+template <int NW, typename V, typename Op>
+__device__ __forceinline__ V block_reduce_n(V v, V* sm, Op op) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v = op(v, __shfl_xor_sync(kFull, v, o));
@@ -185,8 +185,12 @@ __device__ __forceinline__ V block_reduce(V v, V* sm, Op op) {
     __syncthreads();
     V r = sm[0];
 #pragma unroll
-    for (int w = 1; w < kWarps; ++w) r = op(r, sm[w]);
+    for (int w = 1; w < NW; ++w) r = op(r, sm[w]);
     return r;
+}
+template <typename V, typename Op>
+__device__ __forceinline__ V block_reduce(V v, V* sm, Op op) {
+    return block_reduce_n<kWarps>(v, sm, op);
 }
 struct OpSum {
     template <typename V>
@@ -212,9 +216,10 @@ __device__ __forceinline__ double warp_scan_incl(double v) {
     return v;
 }
 
-// Block inclusive scan; returns the inclusive prefix and writes the block
-// total.  `sm` needs kWarps slots.
-__device__ __forceinline__ double block_scan_incl(double v, double* sm, double& total) {
+// Block inclusive scan over NW warps; returns the inclusive prefix and writes
+// the block total.  `sm` needs NW slots.
+template <int NW>
+__device__ __forceinline__ double block_scan_incl_n(double v, double* sm, double& total) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     double incl = warp_scan_incl(v);
     __syncthreads();
@@ -224,9 +229,12 @@ __device__ __forceinline__ double block_scan_incl(double v, double* sm, double& 
     for (int w = 0; w < warp; ++w) off += sm[w];
     double tot = 0.0;
 #pragma unroll
-    for (int w = 0; w < kWarps; ++w) tot += sm[w];
+    for (int w = 0; w < NW; ++w) tot += sm[w];
     total = tot;
     return off + incl;
+}
+__device__ __forceinline__ double block_scan_incl(double v, double* sm, double& total) {
+    return block_scan_incl_n<kWarps>(v, sm, total);
 }
 
 // ---- misaligned-row peeling ---------------------------------------------------

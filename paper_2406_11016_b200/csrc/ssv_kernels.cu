@@ -54,10 +54,11 @@ struct ItemRef {
     int type, b, idx;
 };
 
+constexpr int kMaxWarps = 16;  // block-reduction scratch: 512-thread cluster CTAs
 struct Shared {
-    float fred[kWarps];
-    double dred[kWarps];
-    int ired[kWarps];
+    float fred[kMaxWarps];
+    double dred[kMaxWarps];
+    int ired[kMaxWarps];
     int last;
     unsigned item, item_next;
     Decision dec;
@@ -788,7 +789,7 @@ __device__ void granule(const StepParams& P, int b, int g, const Decision& d, do
 // Inverse CDF of batch row b (whole CTA): granule partials -> SMEM -> fp64
 // granule prefix (contiguous ownership, one scan) -> exact fp64 scan inside
 // the selected granule (dist.cpp:122-137, incl. both fallbacks).
-template <typename T, int ACT>
+template <typename T, int ACT, int NT = kCtaThreads>
 __device__ void locate(const StepParams& P, int b, const Decision& d, Shared& sh, double2* gcache, double u,
                        bool cached = false) {
     const int NG = P.NG, GW = kGW;
@@ -799,7 +800,7 @@ __device__ void locate(const StepParams& P, int b, const Decision& d, Shared& sh
     if (P.trace && b == 0 && threadIdx.x == 0) trace(P, 8 * P.B + 21);
     const int ncache = min(NG, kLocCap);
     if (!cached)
-        for (int g = threadIdx.x; g < ncache; g += kCtaThreads) gcache[g] = __ldcg(&gp[g]);
+        for (int g = threadIdx.x; g < ncache; g += NT) gcache[g] = __ldcg(&gp[g]);
     __syncthreads();
     auto raw = [&](int g) -> double2 { return g < kLocCap ? gcache[g] : __ldcg(&gp[g]); };
 
@@ -915,26 +916,26 @@ __device__ void locate(const StepParams& P, int b, const Decision& d, Shared& sh
 
     // Level 2: exact element scan, continuing into later granules on rounding.
     int token = -1;
-    constexpr int E = (kGW + kCtaThreads - 1) / kCtaThreads;  // elements per thread (2)
-    static_assert(E == 2, "level-2 scan assumes two elements per thread");
+    constexpr int E = (kGW + NT - 1) / NT;  // elements per thread (2 at 256 threads, 1 at 512)
+    static_assert(E == 1 || E == 2, "level-2 scan takes one or two elements per thread");
     while (gstar >= 0 && gstar < NG) {
         const int lo = gstar * GW;
         const int hi = min(lo + GW, P.V);
         const int base = lo + threadIdx.x * E;
         double v0 = 0.0, v1 = 0.0;
         if (base < hi) v0 = exact_value<T, ACT>(P, R, pr, qr, base) / R.denom;
-        if (base + 1 < hi) v1 = exact_value<T, ACT>(P, R, pr, qr, base + 1) / R.denom;
+        if (E > 1 && base + 1 < hi) v1 = exact_value<T, ACT>(P, R, pr, qr, base + 1) / R.denom;
         const double ts = v0 + v1;
         if (tl) trace(P, 8 * P.B + 19);
         double tot;
-        const double incl = block_scan_incl(ts, sh.dred, tot);
+        const double incl = block_scan_incl_n<NT / 32>(ts, sh.dred, tot);
         double cum = carry + (incl - ts);
         int h = 0x7fffffff;
         cum += v0;
         if (base < hi && u < cum) h = base;
         cum += v1;
-        if (h == 0x7fffffff && base + 1 < hi && u < cum) h = base + 1;
-        const int first = block_reduce(h, sh.ired, OpMin());
+        if (h == 0x7fffffff && E > 1 && base + 1 < hi && u < cum) h = base + 1;
+        const int first = block_reduce_n<NT / 32>(h, sh.ired, OpMin());
         if (first != 0x7fffffff) {
             token = first;
             break;
@@ -945,15 +946,15 @@ __device__ void locate(const StepParams& P, int b, const Decision& d, Shared& sh
     if (token < 0) {
         // dist.cpp:135-136: last index with positive mass, else 0.
         int glast = -1;
-        for (int g = threadIdx.x; g < NG; g += kCtaThreads)
+        for (int g = threadIdx.x; g < NG; g += NT)
             if (gmass(g) > 0.0) glast = max(glast, g);
-        glast = block_reduce(glast, sh.ired, OpMax());
+        glast = block_reduce_n<NT / 32>(glast, sh.ired, OpMax());
         token = 0;
         if (glast >= 0) {
             int last = -1;
-            for (int i = glast * GW + threadIdx.x; i < min((glast + 1) * GW, P.V); i += kCtaThreads)
+            for (int i = glast * GW + threadIdx.x; i < min((glast + 1) * GW, P.V); i += NT)
                 if (exact_value<T, ACT>(P, R, pr, qr, i) > 0.0) last = max(last, i);
-            last = block_reduce(last, sh.ired, OpMax());
+            last = block_reduce_n<NT / 32>(last, sh.ired, OpMax());
             if (last >= 0) token = last;
         }
     }
@@ -1141,8 +1142,11 @@ __global__ void __launch_bounds__(kCtaThreads, kCtaMinBlocks) k_verify(StepParam
 //      512-element granule masses;
 //   4. cluster barrier; rank 0 gathers the granule masses through DSMEM and runs
 //      the inverse CDF (locate).
+constexpr int kClThreads = 256;  // cluster CTAs: 8 warps (512 measured slower at C2: two CTAs per SM halve the per-row bandwidth)
+constexpr int kClWarps = kClThreads / 32;
+
 template <typename T, int ACT>
-__global__ void __launch_bounds__(kCtaThreads, 1) k_verify_cluster(StepParams P) {
+__global__ void __launch_bounds__(kClThreads, 1) k_verify_cluster(StepParams P) {
     namespace cg = cooperative_groups;
     constexpr int VEC = Elem<T>::VEC;
     constexpr bool EXACT = ACT == ACT_SOFTMAX;
@@ -1165,6 +1169,7 @@ __global__ void __launch_bounds__(kCtaThreads, 1) k_verify_cluster(StepParams P)
     double2* gcache = gloc + GPS;                                               // [NG] rank 0: all granules
     double* zg = reinterpret_cast<double*>(gcache + P.NG);                     // [3G + 1] gathers, uniforms
     int* offs = reinterpret_cast<int*>(zg + 3 * G + 1);                         // [NS]
+    int* fills = offs + NS;                                                     // [NS] fills issued per slot - 1
 
     const bool tr = P.trace && rank == 0 && tid == 0;  // per-row stamps (tools/trace_step.py)
     if (tr) {
@@ -1182,14 +1187,17 @@ __global__ void __launch_bounds__(kCtaThreads, 1) k_verify_cluster(StepParams P)
     };
     const bool tx = tr && b == 0;  // finer stamps for batch row 0: trace[8B + 2 + k]
     if (EXACT && tid == 0) {
-        for (int i = 0; i < NS; ++i) mbar_init(&full[i], 1);
+        for (int i = 0; i < NS; ++i) {
+            mbar_init(&full[i], 1);
+            fills[i] = 0;
+        }
         mbar_fence_init();
         if (n > 0)
             for (int r = 0; r < NS; ++r) stage_row(r);
     }
     if (tx) trace(P, 8 * P.B + 2);
     // gathers and uniforms (needed by every rank for the decision)
-    for (int c = tid; c < G; c += kCtaThreads) {
+    for (int c = tid; c < G; c += kClThreads) {
         int x = P.ids[(size_t)b * G + c];
         if (x < 0 || x >= V) {
             if (rank == 0) flag(P, SSV_STATUS_TOKEN_RANGE);
@@ -1198,7 +1206,7 @@ __global__ void __launch_bounds__(kCtaThreads, 1) k_verify_cluster(StepParams P)
         zg[c] = load_exact(p_row<T>(P, b, c) + x);
         zg[G + c] = load_exact(q_row<T>(P, b, c) + x);
     }
-    for (int c = tid; c <= G; c += kCtaThreads) {
+    for (int c = tid; c <= G; c += kClThreads) {
         const double u = P.u[(size_t)b * (G + 1) + c];
         zg[2 * G + c] = u;
         if (rank == 0 && P.check_uniforms && (!(u >= 0.0) || !(u < 1.0))) flag(P, SSV_STATUS_UNIFORM_RANGE);
@@ -1211,11 +1219,20 @@ __global__ void __launch_bounds__(kCtaThreads, 1) k_verify_cluster(StepParams P)
         // sum e^(x - max) over the slice, fp32 pairs of <= 16 terms, fp64
         // across.  The warp that consumed a slot restages it with row r + NS.
         float mn = FLT_MAX;
-        for (int r = warp; r < NRc; r += kWarps) {
+        for (int r = warp; r < NRc; r += kClWarps) {
             const int sl = r % NS;
             float m = -FLT_MAX;
             double sd = 0.0;
             if (n > 0) {
+                // Slot reuse: row r is the (r / NS)-th fill of its slot.  Parity
+                // waits only tell the current phase from the one before, so first
+                // make sure the slot's previous row has been consumed (and row r
+                // issued) -- a fresh barrier would otherwise pass a parity-1 wait.
+                if (r >= NS) {
+                    if (lane == 0)
+                        while (ld_volatile_s32(&fills[sl]) < r / NS) __nanosleep(20);
+                    __syncwarp();
+                }
                 mbar_wait(&full[sl], (unsigned)(r / NS) & 1u);
                 const bool txw = P.trace && rank == 0 && b == 0 && lane == 0;
                 if (txw && r < 8) trace(P, 8 * P.B + 4 + r);
@@ -1263,7 +1280,10 @@ __global__ void __launch_bounds__(kCtaThreads, 1) k_verify_cluster(StepParams P)
                 }
                 __syncwarp();
                 if (txw && r < 6) trace(P, 8 * P.B + 12 + r);
-                if (lane == 0 && r + NS < NRc) stage_row(r + NS);  // this warp was the slot's only reader
+                if (lane == 0 && r + NS < NRc) {  // this warp was the slot's only reader
+                    stage_row(r + NS);
+                    st_volatile_s32(&fills[sl], (r + NS) / NS);  // row r + NS is in flight
+                }
             }
             const double S = warp_sum(sd);
             if (lane == 0) {
@@ -1275,7 +1295,7 @@ __global__ void __launch_bounds__(kCtaThreads, 1) k_verify_cluster(StepParams P)
         if (tr) trace(P, 8 * b + 1);
         cl.sync();  // slice partials visible to the cluster
         if (tr) trace(P, 8 * b + 2);
-        for (int r = warp; r < NRc; r += kWarps) {
+        for (int r = warp; r < NRc; r += kClWarps) {
             double2 v = make_double2(-CUDART_INF, 0.0);
             if (lane < CS) v = *cl.map_shared_rank(&part[r], lane);
             const double M = warp_max(v.x);
@@ -1349,7 +1369,7 @@ __global__ void __launch_bounds__(kCtaThreads, 1) k_verify_cluster(StepParams P)
     const Decision d = sh.dec;
     // granule masses of this rank's slice of the needed row(s) (L2-hot re-read)
     if (d.mode != MODE_NONE)
-        for (int j = warp; j < GPS; j += kWarps) {
+        for (int j = warp; j < GPS; j += kClWarps) {
             const int g = rank * GPS + j;
             double2 out = make_double2(0.0, 0.0);
             if (g < P.NG) granule<T, ACT>(P, b, g, d, &out);
@@ -1360,14 +1380,14 @@ __global__ void __launch_bounds__(kCtaThreads, 1) k_verify_cluster(StepParams P)
     if (tr) trace(P, 8 * b + 5);
     if (d.mode == MODE_NONE) return;
     if (rank == 0)
-        for (int g = tid; g < P.NG; g += kCtaThreads) {
+        for (int g = tid; g < P.NG; g += kClThreads) {
             const int k = g / GPS, j = g - k * GPS;
             gcache[g] = *cl.map_shared_rank(&gloc[j], k);
         }
     cl.sync();  // rank 0 is done reading the others' shared memory
     if (rank != 0) return;
     if (tr) trace(P, 8 * b + 6);
-    locate<T, ACT>(P, b, d, sh, gcache, zg[2 * G + G], /*cached=*/true);
+    locate<T, ACT, kClThreads>(P, b, d, sh, gcache, zg[2 * G + G], /*cached=*/true);
     if (tr) {
         trace(P, 8 * b + 7);
         atomicMax(&P.trace[8 * P.B + 1], gtime());
@@ -1629,7 +1649,7 @@ constexpr int kClusterSmemTwoPerSm = 100 * 1024;  // two CTAs per SM (twice the 
 static int cluster_smem(const StepParams& P, int s, int NRc, int NS, int SE, int GPS) {
     const int VEC = 16 / s;
     const int RB = ((SE + 2 * VEC) * s + 15) & ~15;
-    long bytes = (long)NS * RB + 8L * ((NS + 1) & ~1) + 16L * (NRc + GPS + P.NG) + 8L * (3 * P.G + 1) + 4L * NS + 64;
+    long bytes = (long)NS * RB + 8L * ((NS + 1) & ~1) + 16L * (NRc + GPS + P.NG) + 8L * (3 * P.G + 1) + 8L * NS + 64;
     return bytes > kClusterSmemMax ? -1 : (int)bytes;
 }
 
@@ -1642,7 +1662,7 @@ static int max_active_clusters(int cs, int smem) {
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, kClusterSmemMax);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(cs, 1, 1);
-    cfg.blockDim = dim3(kCtaThreads, 1, 1);
+    cfg.blockDim = dim3(kClThreads, 1, 1);
     cfg.dynamicSmemBytes = smem;
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeClusterDimension;
@@ -1722,7 +1742,7 @@ template <typename T, int ACT>
 static void launch_cluster_t(const StepParams& P, const Launch& L) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)(P.B * P.cl_size), 1, 1);
-    cfg.blockDim = dim3(kCtaThreads, 1, 1);
+    cfg.blockDim = dim3(kClThreads, 1, 1);
     cfg.dynamicSmemBytes = P.cl_smem;
     cfg.stream = L.st;
     cudaLaunchAttribute at[1];
