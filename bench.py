@@ -175,6 +175,22 @@ class Workload:
         return step, step, A
 
 
+def acceptance(v, wl):
+    """North star: the sigmoid variant's acceptance-rate deviation from exact
+    softmax on the same inputs and uniforms (mean accepted_len / gamma)."""
+    import numpy as np
+    import torch
+
+    zp, zq, ids, u = wl.sets[0]
+    ex = v.verify_exact(zp, zq, ids, u)
+    sg = v.verify_sigmoid(zp, zq, ids, u, -1e3, 1e3)
+    torch.cuda.synchronize()
+    a = float(np.asarray(ex.accepted_len.cpu()).mean()) / wl.gamma
+    b = float(np.asarray(sg.accepted_len.cpu()).mean()) / wl.gamma
+    same = float((np.asarray(ex.final_token.cpu()) == np.asarray(sg.final_token.cpu())).mean())
+    return {"exact": a, "sigmoid_bounds_1e3": b, "deviation": b - a, "same_final_token_frac": same}
+
+
 def capture(v, wl, steps, stream):
     import torch
 
@@ -454,6 +470,7 @@ def main():
         "gpu_launches": args.steps * m["launches_per_step"],
         "hbm_gbs_step": step_bytes / (ms * 1e-3) / 1e9,
         "accepted_all_rows": A,
+        "acceptance_rate": acceptance(v, wl),
         "e2e": {"value": tokens / e2e_t, "unit": "tokens/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "ms_per_step": e2e_t * 1e3,
                 "path": "ssv_verify_%s_host (C-ABI host entry, pinned host buffers, sync per step)" % args.variant},
