@@ -240,6 +240,9 @@ class Ref(_Base):
         L.ref_verify_sigmoid_sequential.argtypes = vargs + [C.c_double, C.c_double, C.POINTER(_Out)]
         L.ref_verify_sigmoid_fused.argtypes = vargs + [C.c_double, C.c_double, C.c_int, C.c_uint, C.POINTER(_Out)]
         L.ref_make_bench_inputs.argtypes = [C.c_uint64, C.c_int, C.c_int, _dp, _dp, _ip, _dp]
+        L.ref_make_model_pair.argtypes = [C.c_uint64, C.c_int, C.c_double, C.c_double, _dp, _dp]
+        L.ref_decode.argtypes = [_dp, _dp, C.c_int, _ip, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_uint64,
+                                 C.c_int, C.c_double, C.c_double, _ip, _ip, C.POINTER(C.c_int)]
         L.ref_time_backend.argtypes = [C.c_int] + vargs + [
             C.c_double, C.c_double, C.c_int, C.c_uint, C.c_int, C.c_int, _dp, C.POINTER(_Out)]
 
@@ -288,3 +291,27 @@ class Ref(_Base):
         if rc:
             raise ValueError("reference: " + self.lib.ref_last_error().decode())
         return ns, res
+
+    def make_model_pair(self, seed, V, divergence, logit_scale=4.0):
+        """toy_model.cpp:16-42: (target, draft) logit tables, V x V."""
+        t = np.zeros((V, V))
+        d = np.zeros((V, V))
+        if self.lib.ref_make_model_pair(seed, V, divergence, logit_scale, t, d):
+            raise ValueError("reference: " + self.lib.ref_last_error().decode())
+        return t, d
+
+    def decode(self, target, draft, prompt, max_len, gamma=5, min_gamma=1, max_gamma=64, seed=0,
+               backend="reference", alpha=-1e3, beta=1e3):
+        """decode.cpp:45-159 (Backend reference / fused / sigmoid) on the given tables."""
+        V = target.shape[0]
+        target = np.ascontiguousarray(target, np.float64)
+        draft = np.ascontiguousarray(draft, np.float64)
+        prompt = np.ascontiguousarray(prompt, np.int32)
+        tokens = np.zeros(max_len, np.int32)
+        hist = np.zeros(max_len, np.int32)
+        steps = C.c_int(0)
+        code = {"reference": 0, "fused": 1, "sigmoid": 2}[backend]
+        if self.lib.ref_decode(target, draft, V, prompt, prompt.size, max_len, gamma, min_gamma, max_gamma, seed,
+                               code, alpha, beta, tokens, hist, C.byref(steps)):
+            raise ValueError("reference: " + self.lib.ref_last_error().decode())
+        return tokens, hist[:steps.value]

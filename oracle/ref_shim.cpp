@@ -13,6 +13,7 @@
 //   materialize_softmax_into activation.hpp:12-13     / activation.cpp:20-37
 //   verify_sigmoid_*         verify_sigmoid.hpp:41-51 / verify_sigmoid.cpp:50-224
 //   make_bench_inputs        bench.hpp:45             / bench.cpp:46-74
+//   make_model_pair, decode  toy_model.hpp, decode.hpp / toy_model.cpp:16-42, decode.cpp:45-159
 #include <chrono>
 #include <cstdint>
 #include <cstring>
@@ -23,6 +24,8 @@
 
 #include "specsamp/activation.hpp"
 #include "specsamp/bench.hpp"
+#include "specsamp/decode.hpp"
+#include "specsamp/toy_model.hpp"
 #include "specsamp/dist.hpp"
 #include "specsamp/stats.hpp"
 #include "specsamp/step.hpp"
@@ -244,6 +247,42 @@ int ref_time_backend(int backend, const double* zp, int p_steps, const double* z
             }
         }
         copy_result(last, out);
+    });
+}
+
+// toy_model.cpp:16-42: the (target, draft) logit tables, V x V each.
+int ref_make_model_pair(uint64_t seed, int V, double divergence, double logit_scale, double* target,
+                        double* draft) {
+    return guarded([&] {
+        const ModelPair mp = make_model_pair(seed, (size_t)V, divergence, logit_scale);
+        std::memcpy(target, mp.target.table.data(), sizeof(double) * (size_t)V * V);
+        std::memcpy(draft, mp.draft.table.data(), sizeof(double) * (size_t)V * V);
+    });
+}
+
+// decode.cpp:45-159 on given tables (temperature 1).  backend 0 reference,
+// 1 fused, 2 sigmoid.  Writes max_len tokens and the gamma history (max_len
+// entries at most); returns the step count through *steps.
+int ref_decode(const double* target, const double* draft, int V, const int32_t* prompt, int prompt_len,
+               int max_len, int gamma0, int min_gamma, int max_gamma, uint64_t seed, int backend, double alpha,
+               double beta, int32_t* tokens, int32_t* gamma_hist, int* steps) {
+    return guarded([&] {
+        ToyModel t, d;
+        t.vocab_size = d.vocab_size = (size_t)V;
+        t.table.assign(target, target + (size_t)V * V);
+        d.table.assign(draft, draft + (size_t)V * V);
+        DecodeConfig cfg;
+        cfg.max_len = (size_t)max_len;
+        cfg.backend = backend == 0 ? Backend::reference : (backend == 1 ? Backend::fused : Backend::sigmoid);
+        cfg.gamma = GammaState{gamma0, min_gamma, max_gamma};
+        cfg.workers = 2;
+        cfg.bounds = ScaleBounds{alpha, beta};
+        cfg.seed = seed;
+        const DecodeOutput out = decode(t, d, std::span<const int32_t>(prompt, (size_t)prompt_len), cfg);
+        std::memcpy(tokens, out.tokens.data(), sizeof(int32_t) * out.tokens.size());
+        *steps = (int)out.stats.steps;
+        for (size_t i = 0; i < out.stats.gamma_history.size() && i < (size_t)max_len; ++i)
+            gamma_hist[i] = out.stats.gamma_history[i];
     });
 }
 
