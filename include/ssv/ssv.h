@@ -55,6 +55,11 @@ typedef enum { SSV_F32 = 0, SSV_BF16 = 1, SSV_F64 = 2 } ssv_dtype;
 #define SSV_WANT_P 1u
 #define SSV_WANT_Q 2u
 #define SSV_WANT_RESIDUAL 4u
+/* Sigmoid entry points only: binary16 emulation of the activation, exactly
+ * SigmoidStepInputs::emulate_half (dist.cpp:64-69 sigmoid_scaled_value_half:
+ * z, alpha, 1/width, the shifted value, the scaled argument and sigma each
+ * rounded to half) -- the paper's FP16 scale-limit study. */
+#define SSV_EMULATE_HALF 8u
 
 typedef struct ssv_ctx ssv_ctx; /* one per (host thread, device): stream + scratch */
 

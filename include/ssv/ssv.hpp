@@ -127,7 +127,7 @@ struct SigmoidStepInputs {
     LogitTensor z_p;
     LogitTensor z_q;
     ScaleBounds bounds;
-    bool emulate_half = false;  // binary16 emulation is not implemented on the device
+    bool emulate_half = false;  // binary16 emulation (dist.cpp:64-69): SSV_EMULATE_HALF
     Matrix<int32_t> draft_tokens;
     Matrix<double> uniforms;
     size_t batch() const { return z_q.batch(); }
@@ -317,9 +317,8 @@ inline FusedVerifyOutput verify_fused(StepInputs& in, const TilePlan& plan, unsi
 inline VerificationResult verify_sigmoid_sequential(const SigmoidStepInputs& in, Storage storage = Storage::f32,
                                                     Device& dev = default_device()) {
     in.bounds.validate();
-    if (in.emulate_half) throw std::invalid_argument("emulate_half: binary16 emulation is not supported on the device");
     return detail::run(ssv_verify_sigmoid_host, dev.get(), in.z_p, in.z_q, in.draft_tokens, in.uniforms, storage,
-                       in.bounds.alpha, in.bounds.beta);
+                       in.bounds.alpha, in.bounds.beta, in.emulate_half ? SSV_EMULATE_HALF : 0u);
 }
 
 inline FusedVerifyOutput verify_sigmoid_fused(const SigmoidStepInputs& in, const TilePlan& plan, unsigned workers,

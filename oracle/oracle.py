@@ -238,6 +238,7 @@ class Ref(_Base):
         L.ref_verify_exact_logits.argtypes = vargs + [C.POINTER(_Out)]
         L.ref_verify_fused.argtypes = vargs + [C.c_int, C.c_uint, C.POINTER(_Out)]
         L.ref_verify_sigmoid_sequential.argtypes = vargs + [C.c_double, C.c_double, C.POINTER(_Out)]
+        L.ref_verify_sigmoid_sequential_h.argtypes = vargs + [C.c_double, C.c_double, C.c_int, C.POINTER(_Out)]
         L.ref_verify_sigmoid_fused.argtypes = vargs + [C.c_double, C.c_double, C.c_int, C.c_uint, C.POINTER(_Out)]
         L.ref_make_bench_inputs.argtypes = [C.c_uint64, C.c_int, C.c_int, _dp, _dp, _ip, _dp]
         L.ref_make_model_pair.argtypes = [C.c_uint64, C.c_int, C.c_double, C.c_double, _dp, _dp]
@@ -266,6 +267,10 @@ class Ref(_Base):
 
     def verify_sigmoid(self, zp, zq, ids, u, alpha, beta):
         return self._run(self.lib.ref_verify_sigmoid_sequential, zp, zq, ids, u, alpha, beta)
+
+    def verify_sigmoid_half(self, zp, zq, ids, u, alpha, beta):
+        """verify_sigmoid_sequential with emulate_half = true (dist.cpp:64-69)."""
+        return self._run(self.lib.ref_verify_sigmoid_sequential_h, zp, zq, ids, u, alpha, beta, 1)
 
     def verify_sigmoid_fused(self, zp, zq, ids, u, alpha, beta, tile_width=1024, workers=2):
         return self._run(self.lib.ref_verify_sigmoid_fused, zp, zq, ids, u, alpha, beta, tile_width, workers)

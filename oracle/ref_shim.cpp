@@ -156,15 +156,25 @@ int ref_verify_exact_logits(const double* zp, int p_steps, const double* zq, int
     });
 }
 
+int ref_verify_sigmoid_sequential_h(const double* zp, int p_steps, const double* zq, int B,
+                                    int gamma, int V, const int32_t* ids, const double* u,
+                                    double alpha, double beta, int emulate_half, RefOut* out);
+
 int ref_verify_sigmoid_sequential(const double* zp, int p_steps, const double* zq, int B,
                                   int gamma, int V, const int32_t* ids, const double* u,
                                   double alpha, double beta, RefOut* out) {
+    return ref_verify_sigmoid_sequential_h(zp, p_steps, zq, B, gamma, V, ids, u, alpha, beta, 0, out);
+}
+
+int ref_verify_sigmoid_sequential_h(const double* zp, int p_steps, const double* zq, int B,
+                                    int gamma, int V, const int32_t* ids, const double* u,
+                                    double alpha, double beta, int emulate_half, RefOut* out) {
     return guarded([&] {
         SigmoidStepInputs in;
         in.z_p = make_grid(zp, B, p_steps, V);
         in.z_q = make_grid(zq, B, gamma, V);
         in.bounds = ScaleBounds{alpha, beta};
-        in.emulate_half = false;
+        in.emulate_half = emulate_half != 0;
         in.draft_tokens = make_matrix(ids, B, gamma);
         in.uniforms = make_matrix(u, B, gamma + 1);
         copy_result(verify_sigmoid_sequential(in), out);

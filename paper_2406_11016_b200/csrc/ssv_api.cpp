@@ -182,6 +182,7 @@ int run_device(ssv_ctx* ctx, int variant, const ssv_verify_args* a, ssv_verify_o
     P.alpha = a->alpha;
     P.width = a->beta - a->alpha;
     P.check_uniforms = variant != V_SIGMOID;
+    P.emulate_half = variant == V_SIGMOID && (a->flags & SSV_EMULATE_HALF) ? 1 : 0;
     plan_geometry(a->dtype, variant, P);
     if (ctx->path != SSV_PATH_STREAMING) plan_cluster(a->dtype, variant, P);
     const Layout L = plan_scratch(P, 0);

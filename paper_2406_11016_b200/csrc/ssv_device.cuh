@@ -9,6 +9,7 @@
 #pragma once
 
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <math_constants.h>
 #include <stdint.h>
@@ -111,6 +112,17 @@ __device__ __forceinline__ double stable_sigmoid_d(double t) {
 // dist.cpp:60-62 sigmoid_scaled_value: t = (z - alpha) / (beta - alpha).
 __device__ __forceinline__ double sigmoid_scaled_d(double z, double alpha, double width) {
     return stable_sigmoid_d((z - alpha) / width);
+}
+
+// dist.cpp:64-69 sigmoid_scaled_value_half with half.cpp's round_to_half
+// (double -> float -> binary16 RNE -> back): z, alpha, 1/width, the shifted
+// value, the scaled argument and sigma each rounded to half.
+__device__ __forceinline__ double round_half_d(double x) { return (double)__half2float(__float2half_rn((float)x)); }
+__device__ __forceinline__ double sigmoid_half_d(double z, double alpha, double width) {
+    const double inv_w = round_half_d(1.0 / width);
+    const double shifted = round_half_d(round_half_d(z) - round_half_d(alpha));
+    const double arg = round_half_d(shifted * inv_w);
+    return round_half_d(stable_sigmoid_d(arg));
 }
 
 // Streaming-path sigmoid pieces (fp32 or fp64 `acc`).  The sigmoid variant

@@ -98,6 +98,11 @@ __device__ __forceinline__ void trace(const StepParams& P, int idx) {
     if (P.trace) P.trace[idx] = gtime();
 }
 
+// The sigmoid activation as the reference evaluates it (verify_sigmoid.cpp:35-37).
+__device__ __forceinline__ double sigmoid_act(const StepParams& P, double z) {
+    return P.emulate_half ? sigmoid_half_d(z, P.alpha, P.width) : sigmoid_scaled_d(z, P.alpha, P.width);
+}
+
 __device__ __forceinline__ double ratio_clamped(double p, double q) {  // dist.cpp:104-112
     if (q <= kZeroEps) return p > kZeroEps ? 1.0 : 0.0;
     return fmin(1.0, p / q);
@@ -552,8 +557,8 @@ __device__ void decide_gather(const StepParams& P, int b, bool write, Decision& 
             const double zq = load_exact(q_row<T>(P, b, c) + x);
             double p, q;
             if (ACT == ACT_SIGMOID) {
-                p = sigmoid_scaled_d(zp, P.alpha, P.width);
-                q = sigmoid_scaled_d(zq, P.alpha, P.width);
+                p = sigmoid_act(P, zp);
+                q = sigmoid_act(P, zq);
             } else {
                 p = zp;
                 q = zq;
@@ -577,8 +582,8 @@ __device__ void decide_gather(const StepParams& P, int b, bool write, Decision& 
                     const double zq = load_exact(q_row<T>(P, b, c2) + x);
                     double p = zp, q = zq;
                     if (ACT == ACT_SIGMOID) {
-                        p = sigmoid_scaled_d(zp, P.alpha, P.width);
-                        q = sigmoid_scaled_d(zq, P.alpha, P.width);
+                        p = sigmoid_act(P, zp);
+                        q = sigmoid_act(P, zq);
                     } else if (p < 0.0 || q < 0.0) {
                         flag(P, SSV_STATUS_NEGATIVE);
                     }
@@ -630,7 +635,7 @@ struct RowCtx {
 template <int ACT>
 __device__ __forceinline__ double exact_act(const StepParams& P, double z, double M, double S) {
     if (ACT == ACT_SOFTMAX) return exp(z - M) / S;  // dist.cpp:46-50
-    if (ACT == ACT_SIGMOID) return sigmoid_scaled_d(z, P.alpha, P.width);
+    if (ACT == ACT_SIGMOID) return sigmoid_act(P, z);
     return z;
 }
 
@@ -738,6 +743,12 @@ __device__ __forceinline__ double2 granule_reduce(const StepParams& P, const Dec
                 flag(P, SSV_STATUS_NONFINITE);
             return make_double2((double)mx, S);
         }
+        if (ACT == ACT_SIGMOID && P.emulate_half) {  // binary16 emulation: the reference's values, fp64
+            double sh = 0.0;
+            for (int t = 0; t < EPL; ++t)
+                if (t * 32 + lane < n) sh += sigmoid_act(P, (double)D.xs[t]);
+            return make_double2(0.0, warp_sum(sh));
+        }
         A sm = 0;
 #pragma unroll
         for (int t = 0; t < EPL; ++t) {
@@ -747,6 +758,17 @@ __device__ __forceinline__ double2 granule_reduce(const StepParams& P, const Dec
             }
         }
         return make_double2(0.0, warp_sum((double)sm));
+    }
+    if (ACT == ACT_SIGMOID && P.emulate_half) {
+        double ta = 0.0, tp = 0.0;
+        for (int t = 0; t < EPL; ++t) {
+            if (t * 32 + lane < n) {
+                const double vp = sigmoid_act(P, (double)D.xs[t]), vq = sigmoid_act(P, (double)D.xq[t]);
+                ta += vp - vq > 0.0 ? vp - vq : 0.0;
+                tp += vp;
+            }
+        }
+        return make_double2(warp_sum(ta), warp_sum(tp));
     }
     const A Mp = (A)d.Mp, Mq = (A)d.Mq, iSp = (A)(1.0 / d.Sp), iSq = (A)(1.0 / d.Sq);
     A ta = 0, tp = 0;
@@ -1321,8 +1343,8 @@ __global__ void __launch_bounds__(kClThreads, 1) k_verify_cluster(StepParams P) 
                     p = exp(zg[c] - sp.x) / sp.y;  // activation.cpp:20-27, dist.cpp:46-50
                     q = exp(zg[G + c] - sq.x) / sq.y;
                 } else if (ACT == ACT_SIGMOID) {
-                    p = sigmoid_scaled_d(zg[c], P.alpha, P.width);  // dist.cpp:60-62
-                    q = sigmoid_scaled_d(zg[G + c], P.alpha, P.width);
+                    p = sigmoid_act(P, zg[c]);  // dist.cpp:60-69
+                    q = sigmoid_act(P, zg[G + c]);
                 } else {
                     p = zg[c];
                     q = zg[G + c];
@@ -1406,7 +1428,7 @@ __global__ void __launch_bounds__(kThreads) k_materialize(StepParams P, void* ou
     const A alpha = (A)P.alpha, invw = (A)(1.0 / P.width);
     auto act = [&](A x, const double2& st) -> A {
         if (ACT == ACT_SOFTMAX) return exp_rel(x, (A)st.x) * (A)(1.0 / st.y);
-        if (ACT == ACT_SIGMOID) return sigmoid_fast((x - alpha) * invw);
+        if (ACT == ACT_SIGMOID) return P.emulate_half ? (A)sigmoid_act(P, (double)x) : sigmoid_fast((x - alpha) * invw);
         return x;
     };
     auto stat_of = [&](int b, int r) -> double2 {

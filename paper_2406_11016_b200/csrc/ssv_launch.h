@@ -70,6 +70,7 @@ struct StepParams {
     double alpha, width;
     int sample_mode;     // sample softmax(z_p row b) with u[b] (draft sampling)
     int check_uniforms;  // StepInputs::validate checks u in [0,1); the sigmoid variant does not
+    int emulate_half;    // sigmoid: binary16 emulation (SSV_EMULATE_HALF)
     unsigned long long* trace;  // diagnostics: [8*B] per-row phase stamps (tools/trace_step.py), [8*B..+2) kernel start/end
     // scratch
     double2* part;     // [B][NR][K][8] A-item warp partials (max, sum e^(x-max))

@@ -24,6 +24,7 @@ MAKEFILE = os.path.join(PKG_DIR, "csrc", "Makefile")
 SSV_OK, SSV_ECUDA, SSV_EINVAL = 0, 1, 2
 SSV_F32, SSV_BF16, SSV_F64 = 0, 1, 2
 SSV_WANT_P, SSV_WANT_Q, SSV_WANT_RESIDUAL = 1, 2, 4
+SSV_EMULATE_HALF = 8
 
 
 class SsvError(RuntimeError):
@@ -277,7 +278,9 @@ class Verifier:
         """Exact step on device tensors (logits in)."""
         return self._device_call(self.lib.ssv_verify_exact, "ssv_verify_exact", z_p, z_q, ids, u, 0.0, 0.0, flags, out)
 
-    def verify_sigmoid(self, z_p, z_q, ids, u, alpha=-1e3, beta=1e3, flags=0, out=None):
+    def verify_sigmoid(self, z_p, z_q, ids, u, alpha=-1e3, beta=1e3, flags=0, out=None, emulate_half=False):
+        """Sigmoid-approximation step; emulate_half = the reference's binary16 emulation."""
+        flags |= SSV_EMULATE_HALF if emulate_half else 0
         return self._device_call(self.lib.ssv_verify_sigmoid, "ssv_verify_sigmoid", z_p, z_q, ids, u, alpha, beta, flags, out)
 
     def verify_probs(self, p, q, ids, u, flags=0, out=None):
@@ -345,7 +348,9 @@ class Verifier:
         return self._host_call(self.lib.ssv_verify_exact_host, "ssv_verify_exact_host", z_p, z_q, ids, u, 0.0, 0.0,
                                flags, out, dtype)
 
-    def verify_sigmoid_host(self, z_p, z_q, ids, u, alpha=-1e3, beta=1e3, flags=0, out=None, dtype=None):
+    def verify_sigmoid_host(self, z_p, z_q, ids, u, alpha=-1e3, beta=1e3, flags=0, out=None, dtype=None,
+                            emulate_half=False):
+        flags |= SSV_EMULATE_HALF if emulate_half else 0
         return self._host_call(self.lib.ssv_verify_sigmoid_host, "ssv_verify_sigmoid_host", z_p, z_q, ids, u, alpha,
                                beta, flags, out, dtype)
 

@@ -386,3 +386,34 @@ def test_c5_sweep_points(verifier, oracle, gamma, B, V, dtype):
         sub = VerifyResult(r.accepted_len[rows], r.final_token[rows], r.resample_used[rows], r.tau[rows],
                            r.residual_denom[rows])
         assert compare(o, sub, zp, zq, ids, u, kind, label=f"sweep-{kind}-{gamma}-{B}-{V}-{dtype}") <= 1
+
+
+@pytest.mark.parametrize("mag", [1e3, 1e4, 1e5])
+def test_sigmoid_emulate_half(verifier, oracle, ref, mag):
+    """emulate_half = true (dist.cpp:64-69, half.cpp): the binary16-emulated
+    sigmoid against the compiled reference's verify_sigmoid_sequential, up to
+    the paper's +-1e5 failing scale; both kernels."""
+    rng = np.random.default_rng(int(mag))
+    state = (0x4A1F + int(mag), 0)
+    mism = 0
+    for i in range(16):
+        B = int(rng.choice([1, 4, 20]))
+        gamma = int(rng.integers(1, 9))
+        V = int(rng.choice([7, 257, 4099]))
+        bonus = bool(rng.integers(0, 2))
+        (zp, zq, ids, u), state = oracle.make_sigmoid_instance(state, B, gamma, V, bonus, 800.0 if i % 2 else 3.0)
+        zp, zq = oracle.round_f32(zp), oracle.round_f32(zq)
+        o = ref.verify_sigmoid_half(zp, zq, ids, u, -mag, mag)
+        t = to_device(oracle, zp, zq, ids, u, "f32")
+        import torch
+
+        g = verifier.verify_sigmoid(*t, -mag, mag, emulate_half=True)
+        torch.cuda.synchronize()
+        assert int(g.status.item()) == 0
+        gn = g.numpy()
+        assert np.array_equal(gn.accepted_len, o.accepted_len), f"half{i}: accept"
+        assert np.abs(gn.tau - o.tau).max() <= 1e-12, f"half{i}: tau"  # the same binary16 values
+        same = gn.final_token == o.final_token
+        mism += int((~same).sum())
+        assert np.all(np.abs(gn.residual_denom - o.residual_denom) <= 1e-6 * np.maximum(1, np.abs(o.residual_denom)))
+    assert mism <= 1
