@@ -824,6 +824,7 @@ __device__ void locate(const StepParams& P, int b, const Decision& d, Shared& sh
     if (!cached)
         for (int g = threadIdx.x; g < ncache; g += NT) gcache[g] = __ldcg(&gp[g]);
     __syncthreads();
+    const long long cyc0 = clock64();
     auto raw = [&](int g) -> double2 { return g < kLocCap ? gcache[g] : __ldcg(&gp[g]); };
 
     // Level 1 on warp 0 alone (no block barriers): the denominators, then the
@@ -835,6 +836,18 @@ __device__ void locate(const StepParams& P, int b, const Decision& d, Shared& sh
         const int ga = min(NG, lane * gpl), gb = min(NG, ga + gpl);
         bool useA = false;
         double denom = 1.0, gM = 0.0, gS = 1.0;
+        // One pass over the lane's granules and ONE warp scan of unnormalized
+        // masses give both the denominators (the scan totals) and each lane's
+        // prefix; the search then compares against u * denominator (the exact
+        // per-term division happens in level 2).  Short dependency chain: this
+        // runs on one warp between two barriers.
+        double run = 0.0, thr = 0.0;
+        auto wraw = [&](int g) -> double {  // unnormalized granule mass
+            const double2 v = raw(g);
+            if (d.mode == MODE_REJECT) return useA ? v.x : v.y;
+            if (ACT == ACT_SOFTMAX) return v.y > 0.0 ? (g < kLocCap ? v.y : v.y * exp(v.x - gM)) : 0.0;
+            return v.y;
+        };
         if (d.mode == MODE_REJECT) {
             double a1 = 0.0, a2 = 0.0;
             for (int g = ga; g < gb; ++g) {
@@ -842,57 +855,51 @@ __device__ void locate(const StepParams& P, int b, const Decision& d, Shared& sh
                 a1 += v.x;
                 a2 += v.y;
             }
-            const double sa = warp_sum(a1), sp = warp_sum(a2);
+            const double i1 = warp_scan_incl(a1), i2 = warp_scan_incl(a2);
+            const double sa = __shfl_sync(kFull, i1, 31), sp = __shfl_sync(kFull, i2, 31);
             useA = sa > kZeroEps;  // verify_reference.cpp:57-62
             denom = useA ? sa : sp;
+            run = useA ? i1 - a1 : i2 - a2;
             if (lane == 0) {
                 if (P.rsu) P.rsu[b] = 1;
                 if (P.rden) P.rden[b] = useA ? sa : 0.0;
             }
         } else {
+            double sm = 0.0;
             if (ACT == ACT_SOFTMAX) {  // the bonus row's statistics from its granules
                 double m = -CUDART_INF;
                 for (int g = ga; g < gb; ++g) m = fmax(m, raw(g).x);
                 gM = warp_max(m);
-                double sm = 0.0;
                 for (int g = ga; g < gb; ++g) {
                     const double2 v = raw(g);
                     const double w = v.y > 0.0 ? v.y * exp(v.x - gM) : 0.0;
                     sm += w;
                     // rebase the cached granule to the row max: (gM, w) is the same
-                    // mass, and the scans below need no further exp
+                    // mass, and the search below needs no further exp
                     if (g < kLocCap) gcache[g] = make_double2(gM, w);
                 }
-                gS = warp_sum(sm);
             } else {
-                double sm = 0.0;
                 for (int g = ga; g < gb; ++g) sm += raw(g).y;
-                denom = warp_sum(sm);
             }
+            const double incl = warp_scan_incl(sm);
+            const double tot = __shfl_sync(kFull, incl, 31);
+            if (ACT == ACT_SOFTMAX) gS = tot;
+            else denom = tot;
+            run = incl - sm;
             if (lane == 0) {
                 if (P.rsu) P.rsu[b] = 0;
                 if (P.rden) P.rden[b] = 0.0;
             }
         }
-        // Granule masses at granule resolution only pick the granule (the exact
-        // per-term division happens in level 2): a reciprocal is enough here.
-        const double inv = 1.0 / (d.mode != MODE_REJECT && ACT == ACT_SOFTMAX ? gS : denom);
-        auto mass = [&](int g) -> double {
-            const double2 v = raw(g);
-            if (d.mode == MODE_REJECT) return (useA ? v.x : v.y) * inv;
-            if (ACT == ACT_SOFTMAX) return v.y > 0.0 ? (g < kLocCap ? v.y : v.y * exp(v.x - gM)) * inv : 0.0;
-            return v.y * inv;
-        };
-        double tsum = 0.0;
-        for (int g = ga; g < gb; ++g) tsum += mass(g);
-        double run = warp_scan_incl(tsum) - tsum;
+        const double norm = d.mode != MODE_REJECT && ACT == ACT_SOFTMAX ? gS : denom;
+        thr = u * norm;
         int hit = 0x7fffffff;
         double hit_carry = 0.0;
         for (int g = ga; g < gb; ++g) {
-            const double w = mass(g);
-            if (u < run + w) {
+            const double w = wraw(g);
+            if (thr < run + w) {
                 hit = g;
-                hit_carry = run;
+                hit_carry = run / norm;
                 break;
             }
             run += w;
@@ -902,6 +909,9 @@ __device__ void locate(const StepParams& P, int b, const Decision& d, Shared& sh
         const int gst = __shfl_sync(kFull, hit, src);
         const double car = __shfl_sync(kFull, hit_carry, src);
         if (lane == 0) {
+            if (P.trace && b == 0) {
+                P.trace[8 * P.B + 22] = (unsigned long long)(clock64() - cyc0);
+            }
             sh.loc_g = hm ? gst : -1;
             sh.loc_useA = useA;
             sh.loc_d[0] = car;

@@ -52,3 +52,5 @@ lo = t[8 * a.B + 18: 8 * a.B + 22]
 if lo[3] > 0:
     f2 = lambda x: f"{(x - t0) / 1e3:.1f}" if x > 0 else "-"
     print(f"row-0 locate (us): enter {f2(lo[3])} level1-done {f2(lo[0])} level2-values {f2(lo[1])} end {f2(lo[2])}")
+if t[8 * a.B + 22] > 0:
+    print(f"row-0 locate level-1 on warp 0: {int(t[8 * a.B + 22])} cycles")
