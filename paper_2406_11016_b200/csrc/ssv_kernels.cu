@@ -1327,12 +1327,20 @@ __global__ void __launch_bounds__(kClThreads, 1) k_verify_cluster(StepParams P) 
         if (tr) trace(P, 8 * b + 1);
         cl.sync();  // slice partials visible to the cluster
         if (tr) trace(P, 8 * b + 2);
-        for (int r = warp; r < NRc; r += kClWarps) {
+        // Half a warp per row (cl_size <= 16): every row of a small step in one
+        // round, 4-step segmented shuffles, the same fold order on every rank.
+        const int half = lane >> 4, hl = lane & 15;
+        for (int r0 = 2 * warp; r0 < NRc; r0 += 2 * kClWarps) {
+            const int r = r0 + half;
             double2 v = make_double2(-CUDART_INF, 0.0);
-            if (lane < CS) v = *cl.map_shared_rank(&part[r], lane);
-            const double M = warp_max(v.x);
-            const double S = warp_sum(v.y != 0.0 ? v.y * exp(v.x - M) : 0.0);  // NaN propagates
-            if (lane == 0) {
+            if (r < NRc && hl < CS) v = *cl.map_shared_rank(&part[r], hl);
+            double M = v.x;
+#pragma unroll
+            for (int o = 8; o > 0; o >>= 1) M = fmax(M, __shfl_xor_sync(kFull, M, o, 16));
+            double S = v.y != 0.0 ? v.y * exp(v.x - M) : 0.0;  // NaN propagates
+#pragma unroll
+            for (int o = 8; o > 0; o >>= 1) S += __shfl_xor_sync(kFull, S, o, 16);
+            if (hl == 0 && r < NRc) {
                 if (!isfinite(M) || !isfinite(S)) flag(P, SSV_STATUS_NONFINITE);
                 if (r < kMaxRowsSmem) sh.rs[r] = make_double2(M, S);
                 if (rank == 0 && r < P.NR) P.rowstat[(size_t)b * P.NR + r] = make_double2(M, S);
