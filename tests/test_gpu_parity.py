@@ -158,15 +158,20 @@ def test_degenerate_residual_fallback(verifier, oracle):
 
 
 def test_edge_shapes(verifier, oracle):
-    """V = 1, gamma = 1; gamma > 32 (multi-warp acceptance scan); B = 300, V = 5."""
+    """V = 1, gamma = 1; gamma > 32 (multi-warp acceptance scan); gamma > 47 (row
+    statistics beyond the decision's SMEM cache) and > 256 (beyond one thread per
+    position; streaming kernel); B = 300, V = 5."""
     state = (0xED6E, 0)
     for B, gamma, V, bonus in [(1, 1, 1, True), (2, 1, 1, False), (1, 40, 64, True), (300, 2, 5, True),
-                               (3, 33, 1001, False)]:
+                               (3, 33, 1001, False), (2, 64, 300, True), (1, 300, 40, True), (20, 70, 129, False)]:
         (zp, zq, ids, u), state = oracle.make_logit_instance(state, B, gamma, V, bonus, 3.0)
         zp, zq = oracle.round_f32(zp), oracle.round_f32(zq)
         o = oracle.verify_exact(zp, zq, ids, u)
         g = _run(verifier, "exact", *to_device(oracle, zp, zq, ids, u, "f32"))
         assert compare(o, g, zp, zq, ids, u, "exact", label=f"edge{B}-{gamma}-{V}") == 0
+        o = oracle.verify_sigmoid(zp, zq, ids, u, -1e3, 1e3)
+        g = _run(verifier, "sigmoid", *to_device(oracle, zp, zq, ids, u, "f32"))
+        assert compare(o, g, zp, zq, ids, u, "sigmoid", label=f"edge-sig{B}-{gamma}-{V}") == 0
 
 
 def test_misaligned_device_pointers(verifier, oracle):
