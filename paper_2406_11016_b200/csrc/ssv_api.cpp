@@ -183,8 +183,9 @@ int run_device(ssv_ctx* ctx, int variant, const ssv_verify_args* a, ssv_verify_o
     P.width = a->beta - a->alpha;
     P.check_uniforms = variant != V_SIGMOID;
     P.emulate_half = variant == V_SIGMOID && (a->flags & SSV_EMULATE_HALF) ? 1 : 0;
-    plan_geometry(a->dtype, variant, P);
-    if (ctx->path != SSV_PATH_STREAMING) plan_cluster(a->dtype, variant, P);
+    const int act = P.emulate_half ? ACT_SIGMOID_HALF : variant;  // the emulation has its own kernels
+    plan_geometry(a->dtype, act, P);
+    if (ctx->path != SSV_PATH_STREAMING) plan_cluster(a->dtype, act, P);
     const Layout L = plan_scratch(P, 0);
     rc = ensure_scratch(ctx, L.total, (size_t)P.B);
     if (rc) return rc;
@@ -197,7 +198,7 @@ int run_device(ssv_ctx* ctx, int variant, const ssv_verify_args* a, ssv_verify_o
     P.status = o->status ? o->status : ctx->status_dev;
     P.trace = (ctx->trace && trace_slots(P) <= ctx->trace_cap) ? ctx->trace : nullptr;
     ctx->launches = 0;
-    launch_verify(a->dtype, variant, P, want_p ? o->p : nullptr, (a->flags & SSV_WANT_Q) ? o->q : nullptr,
+    launch_verify(a->dtype, act, P, want_p ? o->p : nullptr, (a->flags & SSV_WANT_Q) ? o->q : nullptr,
                   (a->flags & SSV_WANT_RESIDUAL) ? o->residual : nullptr, ctx->launcher());
     CK(cudaGetLastError());
     return SSV_OK;

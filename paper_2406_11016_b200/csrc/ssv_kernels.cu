@@ -99,8 +99,10 @@ __device__ __forceinline__ void trace(const StepParams& P, int idx) {
 }
 
 // The sigmoid activation as the reference evaluates it (verify_sigmoid.cpp:35-37).
+template <int ACT>
 __device__ __forceinline__ double sigmoid_act(const StepParams& P, double z) {
-    return P.emulate_half ? sigmoid_half_d(z, P.alpha, P.width) : sigmoid_scaled_d(z, P.alpha, P.width);
+    if constexpr (ACT == ACT_SIGMOID_HALF) return sigmoid_half_d(z, P.alpha, P.width);
+    return sigmoid_scaled_d(z, P.alpha, P.width);
 }
 
 __device__ __forceinline__ double ratio_clamped(double p, double q) {  // dist.cpp:104-112
@@ -556,9 +558,9 @@ __device__ void decide_gather(const StepParams& P, int b, bool write, Decision& 
             const double zp = load_exact(p_row<T>(P, b, c) + x);
             const double zq = load_exact(q_row<T>(P, b, c) + x);
             double p, q;
-            if (ACT == ACT_SIGMOID) {
-                p = sigmoid_act(P, zp);
-                q = sigmoid_act(P, zq);
+            if (is_sigmoid(ACT)) {
+                p = sigmoid_act<ACT>(P, zp);
+                q = sigmoid_act<ACT>(P, zq);
             } else {
                 p = zp;
                 q = zq;
@@ -581,9 +583,9 @@ __device__ void decide_gather(const StepParams& P, int b, bool write, Decision& 
                     const double zp = load_exact(p_row<T>(P, b, c2) + x);
                     const double zq = load_exact(q_row<T>(P, b, c2) + x);
                     double p = zp, q = zq;
-                    if (ACT == ACT_SIGMOID) {
-                        p = sigmoid_act(P, zp);
-                        q = sigmoid_act(P, zq);
+                    if (is_sigmoid(ACT)) {
+                        p = sigmoid_act<ACT>(P, zp);
+                        q = sigmoid_act<ACT>(P, zq);
                     } else if (p < 0.0 || q < 0.0) {
                         flag(P, SSV_STATUS_NEGATIVE);
                     }
@@ -635,7 +637,7 @@ struct RowCtx {
 template <int ACT>
 __device__ __forceinline__ double exact_act(const StepParams& P, double z, double M, double S) {
     if (ACT == ACT_SOFTMAX) return exp(z - M) / S;  // dist.cpp:46-50
-    if (ACT == ACT_SIGMOID) return sigmoid_act(P, z);
+    if (is_sigmoid(ACT)) return sigmoid_act<ACT>(P, z);
     return z;
 }
 
@@ -743,27 +745,29 @@ __device__ __forceinline__ double2 granule_reduce(const StepParams& P, const Dec
                 flag(P, SSV_STATUS_NONFINITE);
             return make_double2((double)mx, S);
         }
-        if (ACT == ACT_SIGMOID && P.emulate_half) {  // binary16 emulation: the reference's values, fp64
+        if (ACT == ACT_SIGMOID_HALF) {  // binary16 emulation: the reference's values, fp64
             double sh = 0.0;
-            for (int t = 0; t < EPL; ++t)
-                if (t * 32 + lane < n) sh += sigmoid_act(P, (double)D.xs[t]);
+#pragma unroll
+            for (int t = 0; t < EPL; ++t)  // (unrolled: D stays in registers)
+                if (t * 32 + lane < n) sh += sigmoid_act<ACT>(P, (double)D.xs[t]);
             return make_double2(0.0, warp_sum(sh));
         }
         A sm = 0;
 #pragma unroll
         for (int t = 0; t < EPL; ++t) {
             if (t * 32 + lane < n) {
-                if (ACT == ACT_SIGMOID) sm += sigmoid_fast((D.xs[t] - alpha) * invw);
+                if (is_sigmoid(ACT)) sm += sigmoid_fast((D.xs[t] - alpha) * invw);
                 else sm += D.xs[t];
             }
         }
         return make_double2(0.0, warp_sum((double)sm));
     }
-    if (ACT == ACT_SIGMOID && P.emulate_half) {
+    if (ACT == ACT_SIGMOID_HALF) {
         double ta = 0.0, tp = 0.0;
+#pragma unroll
         for (int t = 0; t < EPL; ++t) {
             if (t * 32 + lane < n) {
-                const double vp = sigmoid_act(P, (double)D.xs[t]), vq = sigmoid_act(P, (double)D.xq[t]);
+                const double vp = sigmoid_act<ACT>(P, (double)D.xs[t]), vq = sigmoid_act<ACT>(P, (double)D.xq[t]);
                 ta += vp - vq > 0.0 ? vp - vq : 0.0;
                 tp += vp;
             }
@@ -781,7 +785,7 @@ __device__ __forceinline__ double2 granule_reduce(const StepParams& P, const Dec
                 vp = exp_rel(xp, Mp) * iSp;
                 const A vq = exp_rel(xqq, Mq) * iSq;
                 a = vp - vq > (A)0 ? vp - vq : (A)0;
-            } else if (ACT == ACT_SIGMOID) {
+            } else if (is_sigmoid(ACT)) {
                 // sigma(tp) - sigma(tq) = sigma(tp) sigma(-tq) (1 - e^-(tp-tq)): no cancellation.
                 const A tp_ = (xp - alpha) * invw, tq_ = (xqq - alpha) * invw;
                 const A dd = (xp - xqq) * invw;
@@ -1360,9 +1364,9 @@ __global__ void __launch_bounds__(kClThreads, 1) k_verify_cluster(StepParams P) 
                     const double2 sp = sh.rs[c], sq = sh.rs[G + c];
                     p = exp(zg[c] - sp.x) / sp.y;  // activation.cpp:20-27, dist.cpp:46-50
                     q = exp(zg[G + c] - sq.x) / sq.y;
-                } else if (ACT == ACT_SIGMOID) {
-                    p = sigmoid_act(P, zg[c]);  // dist.cpp:60-69
-                    q = sigmoid_act(P, zg[G + c]);
+                } else if (is_sigmoid(ACT)) {
+                    p = sigmoid_act<ACT>(P, zg[c]);  // dist.cpp:60-69
+                    q = sigmoid_act<ACT>(P, zg[G + c]);
                 } else {
                     p = zg[c];
                     q = zg[G + c];
@@ -1446,7 +1450,7 @@ __global__ void __launch_bounds__(kThreads) k_materialize(StepParams P, void* ou
     const A alpha = (A)P.alpha, invw = (A)(1.0 / P.width);
     auto act = [&](A x, const double2& st) -> A {
         if (ACT == ACT_SOFTMAX) return exp_rel(x, (A)st.x) * (A)(1.0 / st.y);
-        if (ACT == ACT_SIGMOID) return P.emulate_half ? (A)sigmoid_act(P, (double)x) : sigmoid_fast((x - alpha) * invw);
+        if (is_sigmoid(ACT)) return ACT == ACT_SIGMOID_HALF ? (A)sigmoid_act<ACT>(P, (double)x) : sigmoid_fast((x - alpha) * invw);
         return x;
     };
     auto stat_of = [&](int b, int r) -> double2 {
@@ -1768,11 +1772,13 @@ bool plan_cluster(int dtype, int act, StepParams& P) {
     if (dtype == DT_F32) {
         if (act == ACT_SOFTMAX) return plan_cluster_t<float, ACT_SOFTMAX>(P, 4);
         if (act == ACT_SIGMOID) return plan_cluster_t<float, ACT_SIGMOID>(P, 4);
+        if (act == ACT_SIGMOID_HALF) return plan_cluster_t<float, ACT_SIGMOID_HALF>(P, 4);
         return plan_cluster_t<float, ACT_PROBS>(P, 4);
     }
     if (dtype == DT_BF16) {
         if (act == ACT_SOFTMAX) return plan_cluster_t<__nv_bfloat16, ACT_SOFTMAX>(P, 2);
         if (act == ACT_SIGMOID) return plan_cluster_t<__nv_bfloat16, ACT_SIGMOID>(P, 2);
+        if (act == ACT_SIGMOID_HALF) return plan_cluster_t<__nv_bfloat16, ACT_SIGMOID_HALF>(P, 2);
         return plan_cluster_t<__nv_bfloat16, ACT_PROBS>(P, 2);
     }
     return false;
@@ -1821,6 +1827,9 @@ static void dispatch_verify(int act, const StepParams& P, void* outp, void* outq
     } else if (act == ACT_SIGMOID) {
         launch_step_t<T, ACT_SIGMOID>(P, L);
         if (mat) launch_mat_t<T, ACT_SIGMOID>(P, outp, outq, outr, L);
+    } else if (act == ACT_SIGMOID_HALF) {
+        launch_step_t<T, ACT_SIGMOID_HALF>(P, L);
+        if (mat) launch_mat_t<T, ACT_SIGMOID_HALF>(P, outp, outq, outr, L);
     } else {
         launch_step_t<T, ACT_PROBS>(P, L);
         if (mat) launch_mat_t<T, ACT_PROBS>(P, outp, outq, outr, L);

@@ -11,7 +11,10 @@
 namespace ssv {
 
 enum DType : int { DT_F32 = SSV_F32, DT_BF16 = SSV_BF16, DT_F64 = SSV_F64 };
-enum Act : int { ACT_SOFTMAX = 0, ACT_SIGMOID = 1, ACT_PROBS = 2 };
+enum Act : int { ACT_SOFTMAX = 0, ACT_SIGMOID = 1, ACT_PROBS = 2, ACT_SIGMOID_HALF = 3 };
+// The binary16-emulated sigmoid (SSV_EMULATE_HALF) is its own instantiation so
+// its fp64 emulation code stays out of the fast sigmoid kernels.
+constexpr bool is_sigmoid(int act) { return act == ACT_SIGMOID || act == ACT_SIGMOID_HALF; }
 enum Mode : int { MODE_NONE = 0, MODE_REJECT = 1, MODE_BONUS = 2 };
 
 // Work-item geometry of k_verify (one CTA of kCtaThreads threads per item):
