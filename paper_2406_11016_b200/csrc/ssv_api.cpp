@@ -19,8 +19,6 @@ using namespace ssv;
 struct ssv_ctx {
     int device = 0;
     cudaStream_t own = nullptr;
-    cudaStream_t aux = nullptr;           // host entry points: second copy stream (second copy engine)
-    cudaEvent_t fork = nullptr, join = nullptr;
     cudaStream_t stream = nullptr;
     std::string err;
     int launches = 0;
@@ -41,6 +39,7 @@ struct ssv_ctx {
     int path = SSV_PATH_AUTO;
     unsigned long long* trace = nullptr;  // diagnostics (ssv_debug_trace)
     int trace_cap = 0;
+    uint32_t* status_mirror = nullptr;    // set by run_host for the duration of its launch
     Launch launcher() { return Launch{stream, &launches, profiling ? &prof : nullptr}; }
 };
 
@@ -196,6 +195,7 @@ int run_device(ssv_ctx* ctx, int variant, const ssv_verify_args* a, ssv_verify_o
     P.tau = o->tau;
     P.rden = o->residual_denom;
     P.status = o->status ? o->status : ctx->status_dev;
+    P.status_mirror = ctx->status_mirror;
     P.trace = (ctx->trace && trace_slots(P) <= ctx->trace_cap) ? ctx->trace : nullptr;
     ctx->launches = 0;
     launch_verify(a->dtype, act, P, want_p ? o->p : nullptr, (a->flags & SSV_WANT_Q) ? o->q : nullptr,
@@ -248,9 +248,11 @@ int run_host(ssv_ctx* ctx, int variant, const ssv_verify_args* a, ssv_verify_out
     struct Piece {
         size_t off, bytes;
     };
-    // Device staging: the logits, then ONE block of small inputs (ids, uniforms,
-    // a zeroed status word) and ONE block of small outputs, so a call costs two
-    // big copies + one small H2D + one small D2H (each API call is microseconds).
+    // Device staging: the logits, then ONE block of small inputs (ids,
+    // uniforms, a zeroed status word).  The small outputs are written by the
+    // kernels straight into pinned host memory (mapped, UVA), so a call costs
+    // the logits copies + one small H2D and no D2H copy (a D2H costs ~8 us of
+    // copy-engine latency on the critical path, tools/host_overhead.cpp).
     size_t off = 0;
     auto take = [&](size_t bytes) {
         Piece p{off, bytes};
@@ -261,10 +263,18 @@ int run_host(ssv_ctx* ctx, int variant, const ssv_verify_args* a, ssv_verify_out
     const size_t small0 = off;
     const Piece ids = take(B * G * 4), u = take(B * (G + 1) * 8), st = take(4);
     const size_t small_in = off - small0;
-    const Piece acc = take(B * 4), fin = take(B * 4), rsu = take(B), tau = take(B * G * 8), rden = take(B * 8);
-    const size_t small_all = off - small0;
     const bool wp = a->flags & SSV_WANT_P, wq = a->flags & SSV_WANT_Q, wr = a->flags & SSV_WANT_RESIDUAL;
     const Piece pp = take(wp ? np * os : 0), pq = take(wq ? nq * os : 0), pr = take(wr ? nq * os : 0);
+    // pinned host block: [small inputs][status mirror][small outputs]
+    size_t hoff = small_in;
+    auto htake = [&](size_t bytes) {
+        Piece p{hoff, bytes};
+        hoff = align_up(hoff + bytes);
+        return p;
+    };
+    const Piece hst = htake(4), acc = htake(B * 4), fin = htake(B * 4), rsu = htake(B), tau = htake(B * G * 8),
+                rden = htake(B * 8);
+    const size_t hbytes = hoff;
     if (off > ctx->stage_bytes) {
         CK(cudaStreamSynchronize(ctx->stream));
         if (ctx->stage) CK(cudaFree(ctx->stage));
@@ -272,63 +282,56 @@ int run_host(ssv_ctx* ctx, int variant, const ssv_verify_args* a, ssv_verify_out
         CK(cudaMalloc(&ctx->stage, off));
         ctx->stage_bytes = off;
     }
-    if (small_all > ctx->hstage_bytes) {
+    if (hbytes > ctx->hstage_bytes) {
         CK(cudaStreamSynchronize(ctx->stream));
         if (ctx->hstage) CK(cudaFreeHost(ctx->hstage));
         ctx->hstage = nullptr;
-        CK(cudaMallocHost(&ctx->hstage, small_all));
-        ctx->hstage_bytes = small_all;
+        CK(cudaMallocHost(&ctx->hstage, hbytes));
+        ctx->hstage_bytes = hbytes;
     }
     char* d = static_cast<char*>(ctx->stage);
-    char* h = static_cast<char*>(ctx->hstage);  // mirrors d + small0
+    char* h = static_cast<char*>(ctx->hstage);  // [0, small_in) mirrors d + small0
     std::memcpy(h + (ids.off - small0), a->draft_tokens, ids.bytes);
     std::memcpy(h + (u.off - small0), a->uniforms, u.bytes);
     std::memset(h + (st.off - small0), 0, 4);
+    std::memset(h + hst.off, 0, 4);
     cudaStream_t s = ctx->stream;
-    // z_q goes over a second stream so two copy engines share the link (measured
-    // on B200 / PCIe: 18 MB in 360 us on two streams vs 443 us on one).
-    if (!ctx->aux) {
-        CK(cudaStreamCreateWithFlags(&ctx->aux, cudaStreamNonBlocking));
-        CK(cudaEventCreateWithFlags(&ctx->fork, cudaEventDisableTiming));
-        CK(cudaEventCreateWithFlags(&ctx->join, cudaEventDisableTiming));
-    }
-    CK(cudaEventRecord(ctx->fork, s));
-    CK(cudaStreamWaitEvent(ctx->aux, ctx->fork, 0));
-    CK(cudaMemcpyAsync(d + zq.off, a->z_q, zq.bytes, cudaMemcpyHostToDevice, ctx->aux));
-    CK(cudaEventRecord(ctx->join, ctx->aux));
+    // One stream: measured on B200 / PCIe 5, C2's 18.26 MB cross in 336 us as
+    // two copies on one stream, 343 us split over two streams (copy engines),
+    // and every extra copy costs ~4 us (tools/pcie_bw.cu, tools/host_overhead.cpp).
     CK(cudaMemcpyAsync(d + small0, h, small_in, cudaMemcpyHostToDevice, s));
     CK(cudaMemcpyAsync(d + zp.off, a->z_p, zp.bytes, cudaMemcpyHostToDevice, s));
-    CK(cudaStreamWaitEvent(s, ctx->join, 0));
+    CK(cudaMemcpyAsync(d + zq.off, a->z_q, zq.bytes, cudaMemcpyHostToDevice, s));
     ssv_verify_args da = *a;
     da.z_p = d + zp.off;
     da.z_q = d + zq.off;
     da.draft_tokens = reinterpret_cast<const int32_t*>(d + ids.off);
     da.uniforms = reinterpret_cast<const double*>(d + u.off);
     ssv_verify_out dout{};
-    dout.accepted_len = reinterpret_cast<int32_t*>(d + acc.off);
-    dout.final_token = reinterpret_cast<int32_t*>(d + fin.off);
-    dout.resample_used = reinterpret_cast<uint8_t*>(d + rsu.off);
-    dout.tau = reinterpret_cast<double*>(d + tau.off);
-    dout.residual_denom = reinterpret_cast<double*>(d + rden.off);
+    dout.accepted_len = reinterpret_cast<int32_t*>(h + acc.off);
+    dout.final_token = reinterpret_cast<int32_t*>(h + fin.off);
+    dout.resample_used = reinterpret_cast<uint8_t*>(h + rsu.off);
+    dout.tau = reinterpret_cast<double*>(h + tau.off);
+    dout.residual_denom = reinterpret_cast<double*>(h + rden.off);
     dout.status = reinterpret_cast<uint32_t*>(d + st.off);
     dout.p = wp ? d + pp.off : nullptr;
     dout.q = wq ? d + pq.off : nullptr;
     dout.residual = wr ? d + pr.off : nullptr;
+    ctx->status_mirror = reinterpret_cast<uint32_t*>(h + hst.off);
     rc = run_device(ctx, variant, &da, &dout);
+    ctx->status_mirror = nullptr;
     if (rc) return rc;
-    // status word + every small output in one copy
-    CK(cudaMemcpyAsync(h + (st.off - small0), d + st.off, small_all - (st.off - small0), cudaMemcpyDeviceToHost, s));
     if (wp) CK(cudaMemcpyAsync(o->p, dout.p, pp.bytes, cudaMemcpyDeviceToHost, s));
     if (wq) CK(cudaMemcpyAsync(o->q, dout.q, pq.bytes, cudaMemcpyDeviceToHost, s));
     if (wr) CK(cudaMemcpyAsync(o->residual, dout.residual, pr.bytes, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
-    std::memcpy(o->accepted_len, h + (acc.off - small0), acc.bytes);
-    std::memcpy(o->final_token, h + (fin.off - small0), fin.bytes);
-    std::memcpy(o->resample_used, h + (rsu.off - small0), rsu.bytes);
-    std::memcpy(o->tau, h + (tau.off - small0), tau.bytes);
-    std::memcpy(o->residual_denom, h + (rden.off - small0), rden.bytes);
+    std::memcpy(o->accepted_len, h + acc.off, acc.bytes);
+    std::memcpy(o->final_token, h + fin.off, fin.bytes);
+    std::memcpy(o->resample_used, h + rsu.off, rsu.bytes);
+    std::memcpy(o->tau, h + tau.off, tau.bytes);
+    std::memcpy(o->residual_denom, h + rden.off, rden.bytes);
     uint32_t status;
-    std::memcpy(&status, h + (st.off - small0), 4);
+    std::memcpy(&status, h + hst.off, 4);
     if (o->status) *o->status = status;
     return status_to_rc(ctx, status);
 }
@@ -380,9 +383,6 @@ void ssv_destroy(ssv_ctx* ctx) {
     if (ctx->stage) cudaFree(ctx->stage);
     if (ctx->hstage) cudaFreeHost(ctx->hstage);
     if (ctx->status_host) cudaFreeHost(ctx->status_host);
-    if (ctx->aux) cudaStreamDestroy(ctx->aux);
-    if (ctx->fork) cudaEventDestroy(ctx->fork);
-    if (ctx->join) cudaEventDestroy(ctx->join);
     if (ctx->own) cudaStreamDestroy(ctx->own);
     delete ctx;
 }

@@ -87,7 +87,20 @@ __device__ __forceinline__ const T* stat_row(const StepParams& P, int b, int r) 
     return p_row<T>(P, b, P.G);
 }
 
-__device__ __forceinline__ void flag(const StepParams& P, uint32_t bits) { atomicOr(P.status, bits); }
+__device__ __forceinline__ void flag(const StepParams& P, uint32_t bits) {
+    uint32_t v = atomicOr(P.status, bits) | bits;
+    if (P.status_mirror) {
+        // Pinned host mirror (host entry points): bits only accumulate, so
+        // rewrite until the mirror holds the device word's current value.
+        for (;;) {
+            *reinterpret_cast<volatile uint32_t*>(P.status_mirror) = v;
+            __threadfence_system();
+            const uint32_t w = *reinterpret_cast<volatile uint32_t*>(P.status);
+            if (w == v) break;
+            v = w;
+        }
+    }
+}
 
 __device__ __forceinline__ unsigned long long gtime() {
     unsigned long long t;

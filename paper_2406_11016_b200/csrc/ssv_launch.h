@@ -92,6 +92,7 @@ struct StepParams {
     double* tau;
     double* rden;
     uint32_t* status;
+    uint32_t* status_mirror;  // host entry points: pinned host copy of *status (no D2H copy)
 };
 
 // Kernel ids for the profiling hook (ssv_profile_*).

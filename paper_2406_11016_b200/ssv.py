@@ -344,6 +344,40 @@ class Verifier:
         self._check(fn(self.ctx, C.byref(a), C.byref(o)), what)
         return out
 
+    def prepare_host(self, variant, z_p, z_q, ids, u, out, alpha=-1e3, beta=1e3, flags=0, dtype=None):
+        """A reusable host-entry step over fixed (pinned) host buffers: the
+        serving-loop form of verify_*_host.  The returned callable re-runs the
+        C-ABI host entry point on whatever the buffers hold when it is called
+        (argument structs built once; the buffers must stay alive and keep
+        their shapes).  Returns `out` after each call."""
+        fn = {"exact": self.lib.ssv_verify_exact_host, "sigmoid": self.lib.ssv_verify_sigmoid_host,
+              "probs": self.lib.ssv_verify_probs_host}[variant]
+        for name, arr in (("z_p", z_p), ("z_q", z_q), ("ids", ids), ("u", u)):
+            if not arr.flags.c_contiguous:
+                raise ValueError(f"prepare_host: {name} must be C-contiguous")
+        if ids.dtype != np.int32 or u.dtype != np.float64:
+            raise ValueError("prepare_host: ids must be int32 and u float64")
+        B, gamma, V = z_q.shape
+        code = _dtype_code(dtype if dtype is not None else z_q.dtype)
+        if variant != "sigmoid":
+            alpha = beta = 0.0
+        a = Args(B, gamma, V, z_p.shape[1], code, z_p.ctypes.data, z_q.ctypes.data, ids.ctypes.data,
+                 u.ctypes.data, alpha, beta, flags)
+        o = Out(*(getattr(out, f).ctypes.data if getattr(out, f) is not None else None
+                  for f in ("accepted_len", "final_token", "resample_used", "tau", "residual_denom",
+                            "p", "q", "residual", "status")))
+        keep = (z_p, z_q, ids, u, out, a, o)
+        ctx, pa, po, check, what = self.ctx, C.byref(a), C.byref(o), self._check, f"ssv_verify_{variant}_host"
+        if self._follow_torch:
+            self.lib.ssv_set_stream(self.ctx, C.c_void_p(self._own_stream))
+
+        def step():
+            rc = fn(ctx, pa, po)
+            if rc:
+                check(rc, what)
+            return keep[4]
+        return step
+
     def verify_exact_host(self, z_p, z_q, ids, u, flags=0, out=None, dtype=None):
         return self._host_call(self.lib.ssv_verify_exact_host, "ssv_verify_exact_host", z_p, z_q, ids, u, 0.0, 0.0,
                                flags, out, dtype)

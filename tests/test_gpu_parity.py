@@ -252,6 +252,39 @@ def test_host_entry_points_and_errors(verifier, oracle):
     assert compare(o, h, zp, zq, ids, u, "exact") == 0
 
 
+@pytest.mark.parametrize("B,gamma,V", [(2, 5, 32000), (64, 8, 32000)])
+def test_prepared_host_step(verifier, oracle, B, gamma, V):
+    """Verifier.prepare_host over pinned buffers: results follow the buffer
+    contents call by call, device errors (status word mirrored into pinned
+    memory by the kernels) raise, and the step recovers."""
+    from paper_2406_11016_b200 import SsvInvalidArgument
+    from paper_2406_11016_b200.ssv import VerifyResult
+
+    hzp = verifier.host_empty((B, gamma + 1, V), np.float32)
+    hzq = verifier.host_empty((B, gamma, V), np.float32)
+    hids = verifier.host_empty((B, gamma), np.int32)
+    hu = verifier.host_empty((B, gamma + 1), np.float64)
+    out = VerifyResult(verifier.host_empty((B,), np.int32), verifier.host_empty((B,), np.int32),
+                       verifier.host_empty((B,), np.uint8), verifier.host_empty((B, gamma), np.float64),
+                       verifier.host_empty((B,), np.float64), status=verifier.host_empty((1,), np.uint32))
+    step = verifier.prepare_host("exact", hzp, hzq, hids, hu, out)
+    for seed in (3, 11):
+        zp, zq, ids, u = oracle.make_bench_batch(seed, B, gamma, V)
+        zp, zq = oracle.round_f32(zp), oracle.round_f32(zq)
+        hzp[...], hzq[...], hids[...], hu[...] = zp, zq, ids, u
+        r = step()
+        assert compare(oracle.verify_exact(zp, zq, ids, u), r, zp, zq, ids, u, "exact") == 0
+        assert r.status[0] == 0
+    hzq[B - 1, gamma - 1, V // 2] = np.nan
+    with pytest.raises(SsvInvalidArgument, match="non-finite"):
+        step()
+    assert out.status[0] & 1
+    hzq[B - 1, gamma - 1, V // 2] = zq[B - 1, gamma - 1, V // 2]
+    r = step()
+    assert r.status[0] == 0
+    assert compare(oracle.verify_exact(zp, zq, ids, u), r, zp, zq, ids, u, "exact") == 0
+
+
 def test_determinism(verifier, oracle):
     zp, zq, ids, u = oracle.make_bench_batch(9, 16, 8, 51865)
     zp, zq = oracle.round_f32(zp), oracle.round_f32(zq)
