@@ -87,6 +87,16 @@ __device__ __forceinline__ const T* stat_row(const StepParams& P, int b, int r) 
     return p_row<T>(P, b, P.G);
 }
 
+// Programmatic dependent launch: the verify kernels are launched with
+// programmatic stream serialization, so the next kernel's CTAs may be
+// scheduled while this grid drains (its launch latency overlaps our tail).
+// Every CTA releases its dependents at entry and waits for its own
+// predecessor's completion (and memory flush) before touching anything.
+__device__ __forceinline__ void pdl_enter() {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+
 __device__ __forceinline__ void flag(const StepParams& P, uint32_t bits) {
     uint32_t v = atomicOr(P.status, bits) | bits;
     if (P.status_mirror) {
@@ -1118,6 +1128,7 @@ __global__ void __launch_bounds__(kCtaThreads, kCtaMinBlocks) k_verify(StepParam
     __shared__ Shared sh;
     extern __shared__ __align__(128) uint4 dsm[];
     const int tid = threadIdx.x;
+    pdl_enter();
     if (P.trace && blockIdx.x == 0 && tid == 0) trace(P, 8 * P.B);
     // Claims run two ahead: the item after the current one is known while the
     // current one runs (an A-run streams its first chunks early), and the
@@ -1202,6 +1213,7 @@ __global__ void __launch_bounds__(kClThreads, 1) k_verify_cluster(StepParams P) 
     cg::cluster_group cl = cg::this_cluster();
     __shared__ Shared sh;
     extern __shared__ __align__(128) uint8_t csm[];
+    pdl_enter();
     const int CS = P.cl_size, SE = P.cl_se, GPS = P.cl_gps, RB = P.cl_rowbytes;
     const int rank = (int)cl.block_rank();
     const int b = blockIdx.x / CS;
@@ -1212,8 +1224,9 @@ __global__ void __launch_bounds__(kClThreads, 1) k_verify_cluster(StepParams P) 
     const int NS = EXACT ? P.cl_slots : 1;  // ring slots (NS == NRc: every row resident at once)
     // shared-memory carve-up (host: cluster_smem)
     uint8_t* slots = csm;                                                       // NS x RB
+    const int NSp = (NS + 1) & ~1;
     uint64_t* full = reinterpret_cast<uint64_t*>(slots + (size_t)NS * RB);      // NS (even-padded)
-    double2* part = reinterpret_cast<double2*>(full + ((NS + 1) & ~1));         // [NRc] slice partials (DSMEM)
+    double2* part = reinterpret_cast<double2*>(full + NSp);                     // [NRc] slice partials (DSMEM)
     double2* gloc = part + NRc;                                                 // [GPS] granule partials (DSMEM)
     double2* gcache = gloc + GPS;                                               // [NG] rank 0: all granules
     double* zg = reinterpret_cast<double*>(gcache + P.NG);                     // [3G + 1] gathers, uniforms
@@ -1264,9 +1277,11 @@ __global__ void __launch_bounds__(kClThreads, 1) k_verify_cluster(StepParams P) 
     if (tx) trace(P, 8 * P.B + 3);
 
     if constexpr (EXACT) {
-        // One warp per row slice (rows in flight in parallel): max, then
-        // sum e^(x - max) over the slice, fp32 pairs of <= 16 terms, fp64
-        // across.  The warp that consumed a slot restages it with row r + NS.
+        // One warp per row slice (rows in flight in parallel): per-lane online
+        // max / sum of e^(x - max) in one pass over the slot; the warp that
+        // consumed a slot restages it with row r + NS.  (Tried: the whole CTA
+        // on one row at a time, rows in ring order -- ~1.5x slower at C1/C2:
+        // the per-row warp folds then sit on the critical path.)
         float mn = FLT_MAX;
         for (int r = warp; r < NRc; r += kClWarps) {
             const int sl = r % NS;
@@ -1287,9 +1302,14 @@ __global__ void __launch_bounds__(kClThreads, 1) k_verify_cluster(StepParams P) 
                 if (txw && r < 8) trace(P, 8 * P.B + 4 + r);
                 const int off = offs[sl], nv = (off + n + VEC - 1) / VEC;
                 const uint4* rv = reinterpret_cast<const uint4*>(slots + (size_t)sl * RB);
-                // Interior vectors [1, nv - 1) in the main loops, unmasked, four
-                // independent accumulator chains per lane (the loops are latency-
-                // bound at 8 warps per SM); the two edge vectors are masked apart.
+                // A step loads 4 vectors per lane (unguarded in the interior, so
+                // the 4 shared-memory loads are in flight together), takes their
+                // max, rescales the lane's sums if the max grew, and adds the
+                // step's terms.  The sums stay fp32 (four chains per lane, <= 4
+                // terms per chain per step; fp64 only in the lane / slice /
+                // cluster folds): fp64 adds in the loop cost ~1.8x the slice
+                // time (tools/slice_bench.cu).  The two edge vectors are masked
+                // and join the last step.
                 auto edge = [&](int v) {
                     uint4 w = rv[v];
                     if (v == 0 && off) mask_vec<T>(w, off, VEC);
@@ -1297,36 +1317,40 @@ __global__ void __launch_bounds__(kClThreads, 1) k_verify_cluster(StepParams P) 
                     return w;
                 };
                 const int vi1 = max(1, nv - 1);
-                float mk[4] = {-FLT_MAX, -FLT_MAX, -FLT_MAX, -FLT_MAX}, nk[4] = {FLT_MAX, FLT_MAX, FLT_MAX, FLT_MAX};
-                if (!(P.dbg & 1)) {
-                    for (int v0 = 1 + lane; v0 < vi1; v0 += 128) {
+                float2 s0 = make_float2(0.f, 0.f), s1 = make_float2(0.f, 0.f);
+                auto step = [&](const uint4* w, int nw) {
+                    float cm = -FLT_MAX;
 #pragma unroll
-                        for (int u = 0; u < 4; ++u)
-                            if (v0 + 32 * u < vi1) AStat<T>::minmax(rv[v0 + 32 * u], mk[u], nk[u]);
+                    for (int u = 0; u < 5; ++u)
+                        if (u < nw) AStat<T>::minmax(w[u], cm, mn);
+                    if (cm > m) {
+                        const float f = ex2f((m - cm) * 1.4426950408889634f);  // 0 on the first step
+                        s0 = __fmul2_rn(s0, make_float2(f, f));
+                        s1 = __fmul2_rn(s1, make_float2(f, f));
+                        m = cm;
                     }
-                    if (lane == 0) AStat<T>::minmax(edge(0), mk[0], nk[0]);
-                    if (lane == 1 && nv > 1) AStat<T>::minmax(edge(nv - 1), mk[1], nk[1]);
-                }
-                m = fmaxf(fmaxf(mk[0], mk[1]), fmaxf(mk[2], mk[3]));
-                mn = fminf(mn, fminf(fminf(nk[0], nk[1]), fminf(nk[2], nk[3])));
-                m = warp_max(m);
-                if (m != -FLT_MAX && !(P.dbg & 2)) {
-                    const float2 negM = make_float2(-m, -m);
-                    for (int v0 = 1 + lane; v0 < vi1; v0 += 128) {
-                        float2 sk[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
-                                        make_float2(0.f, 0.f)};
+                    if (m != -FLT_MAX) {  // a lane that has seen pads only adds nothing
+                        const float2 negM = make_float2(-m, -m);
 #pragma unroll
-                        for (int u = 0; u < 4; ++u)
-                            if (v0 + 32 * u < vi1) AStat<T>::expsum(rv[v0 + 32 * u], negM, sk[u]);
-                        // fp32 tree over the <= 16 terms of this step, then one fp64 add per pair lane
-                        const float2 t = __fadd2_rn(__fadd2_rn(sk[0], sk[1]), __fadd2_rn(sk[2], sk[3]));
-                        sd += (double)t.x + (double)t.y;
+                        for (int u = 0; u < 5; ++u)
+                            if (u < nw) AStat<T>::expsum(w[u], negM, (u & 1) ? s1 : s0);
                     }
-                    float2 se = make_float2(0.f, 0.f);
-                    if (lane == 0) AStat<T>::expsum(edge(0), negM, se);
-                    if (lane == 1 && nv > 1) AStat<T>::expsum(edge(nv - 1), negM, se);
-                    sd += (double)se.x + (double)se.y;
+                };
+                int v0 = 1 + lane;
+                for (; v0 + 96 < vi1; v0 += 128) {
+                    uint4 w[4];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) w[u] = rv[v0 + 32 * u];
+                    step(w, 4);
                 }
+                {  // the remainder (< 4 vectors per lane) and the edge vectors
+                    uint4 w[5];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) w[u] = v0 + 32 * u < vi1 ? rv[v0 + 32 * u] : pad_vec<T>();
+                    w[4] = lane == 0 ? edge(0) : (lane == 1 && nv > 1 ? edge(nv - 1) : pad_vec<T>());
+                    step(w, 5);
+                }
+                sd = ((double)s0.x + (double)s0.y) + ((double)s1.x + (double)s1.y);
                 __syncwarp();
                 if (txw && r < 6) trace(P, 8 * P.B + 12 + r);
                 if (lane == 0 && r + NS < NRc) {  // this warp was the slot's only reader
@@ -1334,10 +1358,13 @@ __global__ void __launch_bounds__(kClThreads, 1) k_verify_cluster(StepParams P) 
                     st_volatile_s32(&fills[sl], (r + NS) / NS);  // row r + NS is in flight
                 }
             }
-            const double S = warp_sum(sd);
+            // fold the lanes: M = max, S = sum of s_l e^(m_l - M) (fp64)
+            const float M = warp_max(m);
+            double S = sd != 0.0 ? sd * exp((double)m - (double)M) : sd;  // NaN propagates
+            S = warp_sum(S);
             if (lane == 0) {
-                if (isnan(S) || m == INFINITY) flag(P, SSV_STATUS_NONFINITE);
-                part[r] = S != 0.0 ? make_double2((double)m, S) : make_double2(-CUDART_INF, 0.0);
+                if (isnan(S) || M == INFINITY) flag(P, SSV_STATUS_NONFINITE);
+                part[r] = S != 0.0 ? make_double2((double)M, S) : make_double2(-CUDART_INF, 0.0);
             }
         }
         if (__any_sync(kFull, isinf(mn)) && lane == 0) flag(P, SSV_STATUS_NONFINITE);
@@ -1674,6 +1701,15 @@ void plan_geometry(int dtype, int act, StepParams& P) {
 
 int trace_slots(const StepParams& P) { return 8 * P.B + 26; }
 
+// Programmatic stream serialization for the verify launches (see pdl_enter).
+static int pdl_attr(cudaLaunchAttribute& a) {
+    static const bool off = getenv("SSV_NO_PDL") != nullptr;  // experiment knob
+    if (off) return 0;
+    a.id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    a.val.programmaticStreamSerializationAllowed = 1;
+    return 1;
+}
+
 template <typename T, int ACT>
 static void launch_verify_t(const StepParams& P, const Launch& L) {
     static bool attr = false;
@@ -1693,8 +1729,16 @@ static void launch_verify_t(const StepParams& P, const Launch& L) {
     Q.claim_ahead = P.n_items > 2u * grid;
     static const int dbgm = getenv("SSV_DBG_MODE") ? atoi(getenv("SSV_DBG_MODE")) : 0;
     Q.dbg = dbgm;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid, 1, 1);
+    cfg.blockDim = dim3(kCtaThreads, 1, 1);
+    cfg.dynamicSmemBytes = kDynSmem;
+    cfg.stream = L.st;
+    cudaLaunchAttribute at[1];
+    cfg.attrs = at;
+    cfg.numAttrs = pdl_attr(at[0]);
     const int h = L.begin(KID_VERIFY);
-    k_verify<T, ACT><<<grid, kCtaThreads, kDynSmem, L.st>>>(Q);
+    cudaLaunchKernelEx(&cfg, k_verify<T, ACT>, Q);
     L.end(h);
 }
 
@@ -1804,13 +1848,13 @@ static void launch_cluster_t(const StepParams& P, const Launch& L) {
     cfg.blockDim = dim3(kClThreads, 1, 1);
     cfg.dynamicSmemBytes = P.cl_smem;
     cfg.stream = L.st;
-    cudaLaunchAttribute at[1];
+    cudaLaunchAttribute at[2];
     at[0].id = cudaLaunchAttributeClusterDimension;
     at[0].val.clusterDim.x = P.cl_size;
     at[0].val.clusterDim.y = 1;
     at[0].val.clusterDim.z = 1;
     cfg.attrs = at;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = 1 + pdl_attr(at[1]);
     const int h = L.begin(KID_VERIFY);
     cudaLaunchKernelEx(&cfg, k_verify_cluster<T, ACT>, P);
     L.end(h);
