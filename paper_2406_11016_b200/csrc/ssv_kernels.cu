@@ -1792,13 +1792,21 @@ static bool plan_cluster_t(StepParams& P, int s) {
     static const bool dbg = getenv("SSV_DEBUG") != nullptr;
     if (off || P.sample_mode || P.G > 256 || P.NG > kLocCap) return false;
     const int NRc = ACT == ACT_SOFTMAX ? 2 * P.G + (P.NR > 2 * P.G ? 1 : 0) : 0;  // bonus stats only if materialized
-    for (int cs : {16, 12, 8}) {
+    if (NRc > kMaxRowsSmem) return false;  // the decision reads every row's statistics from SMEM
+    // (two-CTA clusters measured slower than the streaming kernel at B = 64)
+    for (int cs : {16, 12, 8, 4}) {
         const int SE = ((P.V + cs - 1) / cs + kGW - 1) / kGW * kGW;
         const int GPS = SE / kGW;
         const int RB = NRc > 0 ? ((SE + 2 * (16 / s)) * s + 15) & ~15 : 0;
+        // Measured crossover vs the streaming kernel (tools/sweep.py, gamma 1-16 x
+        // B 1-64 x V 32000-151936): a CTA's slices of all rows must stay small
+        // enough for its shared-memory ring -- ~300 KB, ~520 KB at B >= 48
+        // where the streaming kernel's per-row tail costs more.
+        if ((long)NRc * RB > (P.B >= 48 ? 520L : 300L) * 1024) continue;
         // every row resident if that still leaves two CTAs per SM, else a ring
         int NS = NRc;
-        if (NS > 0 && cluster_smem(P, s, NRc, NS, SE, GPS) > kClusterSmemTwoPerSm) {
+        const int all_rows = NS > 0 ? cluster_smem(P, s, NRc, NS, SE, GPS) : 0;  // -1: beyond one SM
+        if (all_rows < 0 || all_rows > kClusterSmemTwoPerSm) {
             const int base = cluster_smem(P, s, NRc, 0, SE, GPS);
             NS = std::max(2, std::min(NRc, (kClusterSmemTwoPerSm - base) / std::max(RB + 20, 1)));
         }
