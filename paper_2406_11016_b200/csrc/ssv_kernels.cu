@@ -835,21 +835,74 @@ __device__ void granule(const StepParams& P, int b, int g, const Decision& d, do
 }
 
 // ---------------------------------------------------------------------------
+// Inverse CDF, element level (whole CTA): exact fp64 scan from granule gstar
+// with the cumulative mass `carry` before it, continuing into later granules
+// on rounding; no hit -> dist.cpp:135-136 (last index with positive mass,
+// else 0), with gmass(g) the normalized mass of granule g.  Returns the token.
+template <typename T, int ACT, int NT, typename GMass>
+__device__ int locate_scan(const StepParams& P, const RowCtx& R, const T* pr, const T* qr, int gstar, double carry,
+                           double u, const GMass& gmass, Shared& sh, bool tl) {
+    const int NG = P.NG, GW = kGW;
+    int token = -1;
+    constexpr int E = (kGW + NT - 1) / NT;  // elements per thread (2 at 256 threads, 1 at 512)
+    static_assert(E == 1 || E == 2, "level-2 scan takes one or two elements per thread");
+    while (gstar >= 0 && gstar < NG) {
+        const int lo = gstar * GW;
+        const int hi = min(lo + GW, P.V);
+        const int base = lo + threadIdx.x * E;
+        double v0 = 0.0, v1 = 0.0;
+        if (base < hi) v0 = exact_value<T, ACT>(P, R, pr, qr, base) / R.denom;
+        if (E > 1 && base + 1 < hi) v1 = exact_value<T, ACT>(P, R, pr, qr, base + 1) / R.denom;
+        const double ts = v0 + v1;
+        if (tl) trace(P, 8 * P.B + 19);
+        double tot;
+        const double incl = block_scan_incl_n<NT / 32>(ts, sh.dred, tot);
+        double cum = carry + (incl - ts);
+        int h = 0x7fffffff;
+        cum += v0;
+        if (base < hi && u < cum) h = base;
+        cum += v1;
+        if (h == 0x7fffffff && E > 1 && base + 1 < hi && u < cum) h = base + 1;
+        const int first = block_reduce_n<NT / 32>(h, sh.ired, OpMin());
+        if (first != 0x7fffffff) {
+            token = first;
+            break;
+        }
+        carry += tot;
+        ++gstar;
+    }
+    if (token < 0) {
+        // dist.cpp:135-136: last index with positive mass, else 0.
+        int glast = -1;
+        for (int g = threadIdx.x; g < NG; g += NT)
+            if (gmass(g) > 0.0) glast = max(glast, g);
+        glast = block_reduce_n<NT / 32>(glast, sh.ired, OpMax());
+        token = 0;
+        if (glast >= 0) {
+            int last = -1;
+            for (int i = glast * GW + threadIdx.x; i < min((glast + 1) * GW, P.V); i += NT)
+                if (exact_value<T, ACT>(P, R, pr, qr, i) > 0.0) last = max(last, i);
+            last = block_reduce_n<NT / 32>(last, sh.ired, OpMax());
+            if (last >= 0) token = last;
+        }
+    }
+    return token;
+}
+
+// ---------------------------------------------------------------------------
 // Inverse CDF of batch row b (whole CTA): granule partials -> SMEM -> fp64
 // granule prefix (contiguous ownership, one scan) -> exact fp64 scan inside
 // the selected granule (dist.cpp:122-137, incl. both fallbacks).
 template <typename T, int ACT, int NT = kCtaThreads>
-__device__ void locate(const StepParams& P, int b, const Decision& d, Shared& sh, double2* gcache, double u,
-                       bool cached = false) {
-    const int NG = P.NG, GW = kGW;
-    const double2* gp = P.gpart + (size_t)b * NG;  // (cached: gcache already holds all NG <= kLocCap)
+__device__ void locate(const StepParams& P, int b, const Decision& d, Shared& sh, double2* gcache, double u) {
+    const int NG = P.NG;
+    const double2* gp = P.gpart + (size_t)b * NG;
     const T* pr = p_row<T>(P, b, d.row);
     const T* qr = d.mode == MODE_REJECT ? q_row<T>(P, b, d.row) : nullptr;
     // u = u_final (verify_reference.cpp:98), loaded by the caller ahead of time
     if (P.trace && b == 0 && threadIdx.x == 0) trace(P, 8 * P.B + 21);
     const int ncache = min(NG, kLocCap);
-    if (!cached)
-        for (int g = threadIdx.x; g < ncache; g += NT) gcache[g] = __ldcg(&gp[g]);
+    for (int g = threadIdx.x; g < ncache; g += NT) gcache[g] = __ldcg(&gp[g]);
     __syncthreads();
     const long long cyc0 = clock64();
     auto raw = [&](int g) -> double2 { return g < kLocCap ? gcache[g] : __ldcg(&gp[g]); };
@@ -973,50 +1026,7 @@ __device__ void locate(const StepParams& P, int b, const Decision& d, Shared& sh
     const bool tl = P.trace && b == 0 && threadIdx.x == 0;  // locate stamps: trace[8B + 18 ..]
     if (tl) trace(P, 8 * P.B + 18);
 
-    // Level 2: exact element scan, continuing into later granules on rounding.
-    int token = -1;
-    constexpr int E = (kGW + NT - 1) / NT;  // elements per thread (2 at 256 threads, 1 at 512)
-    static_assert(E == 1 || E == 2, "level-2 scan takes one or two elements per thread");
-    while (gstar >= 0 && gstar < NG) {
-        const int lo = gstar * GW;
-        const int hi = min(lo + GW, P.V);
-        const int base = lo + threadIdx.x * E;
-        double v0 = 0.0, v1 = 0.0;
-        if (base < hi) v0 = exact_value<T, ACT>(P, R, pr, qr, base) / R.denom;
-        if (E > 1 && base + 1 < hi) v1 = exact_value<T, ACT>(P, R, pr, qr, base + 1) / R.denom;
-        const double ts = v0 + v1;
-        if (tl) trace(P, 8 * P.B + 19);
-        double tot;
-        const double incl = block_scan_incl_n<NT / 32>(ts, sh.dred, tot);
-        double cum = carry + (incl - ts);
-        int h = 0x7fffffff;
-        cum += v0;
-        if (base < hi && u < cum) h = base;
-        cum += v1;
-        if (h == 0x7fffffff && E > 1 && base + 1 < hi && u < cum) h = base + 1;
-        const int first = block_reduce_n<NT / 32>(h, sh.ired, OpMin());
-        if (first != 0x7fffffff) {
-            token = first;
-            break;
-        }
-        carry += tot;
-        ++gstar;
-    }
-    if (token < 0) {
-        // dist.cpp:135-136: last index with positive mass, else 0.
-        int glast = -1;
-        for (int g = threadIdx.x; g < NG; g += NT)
-            if (gmass(g) > 0.0) glast = max(glast, g);
-        glast = block_reduce_n<NT / 32>(glast, sh.ired, OpMax());
-        token = 0;
-        if (glast >= 0) {
-            int last = -1;
-            for (int i = glast * GW + threadIdx.x; i < min((glast + 1) * GW, P.V); i += NT)
-                if (exact_value<T, ACT>(P, R, pr, qr, i) > 0.0) last = max(last, i);
-            last = block_reduce_n<NT / 32>(last, sh.ired, OpMax());
-            if (last >= 0) token = last;
-        }
-    }
+    const int token = locate_scan<T, ACT, NT>(P, R, pr, qr, gstar, carry, u, gmass, sh, tl);
     if (tl) trace(P, 8 * P.B + 20);
     if (threadIdx.x == 0) P.fin[b] = token;
 }
@@ -1228,8 +1238,8 @@ __global__ void __launch_bounds__(kClThreads, 1) k_verify_cluster(StepParams P) 
     uint64_t* full = reinterpret_cast<uint64_t*>(slots + (size_t)NS * RB);      // NS (even-padded)
     double2* part = reinterpret_cast<double2*>(full + NSp);                     // [NRc] slice partials (DSMEM)
     double2* gloc = part + NRc;                                                 // [GPS] granule partials (DSMEM)
-    double2* gcache = gloc + GPS;                                               // [NG] rank 0: all granules
-    double* zg = reinterpret_cast<double*>(gcache + P.NG);                     // [3G + 1] gathers, uniforms
+    double2* rtot = gloc + GPS;                                                 // [16] slice totals (pushed by the ranks)
+    double* zg = reinterpret_cast<double*>(rtot + 16);                          // [3G + 1] gathers, uniforms
     int* offs = reinterpret_cast<int*>(zg + 3 * G + 1);                         // [NS]
     int* fills = offs + NS;                                                     // [NS] fills issued per slot - 1
 
@@ -1451,30 +1461,176 @@ __global__ void __launch_bounds__(kClThreads, 1) k_verify_cluster(StepParams P) 
     __syncthreads();
     if (tr) trace(P, 8 * b + 3);
     const Decision d = sh.dec;
-    // granule masses of this rank's slice of the needed row(s) (L2-hot re-read)
-    if (d.mode != MODE_NONE)
+    // Granule masses of this rank's slice of the needed row(s) (L2-hot re-read),
+    // also stored to global for the rare last-positive fallback.  The slice
+    // total (fixed order) is pushed into every rank's rtot[rank] so that after
+    // the barrier each rank holds all totals locally (no DSMEM reads after it).
+    const int nloc = max(0, min(GPS, P.NG - rank * GPS));  // this rank's granules
+    if (d.mode != MODE_NONE) {
         for (int j = warp; j < GPS; j += kClWarps) {
             const int g = rank * GPS + j;
             double2 out = make_double2(0.0, 0.0);
             if (g < P.NG) granule<T, ACT>(P, b, g, d, &out);
-            if (lane == 0) gloc[j] = out;
+            if (lane == 0) {
+                gloc[j] = out;
+                if (g < P.NG) P.gpart[(size_t)b * P.NG + g] = out;
+            }
         }
+        __syncthreads();
+        if (warp == 0) {
+            double2 t;
+            if (d.mode == MODE_BONUS && ACT == ACT_SOFTMAX) {  // (max, sum e^(x - max)) of the slice
+                double m = -CUDART_INF;
+                for (int j = lane; j < nloc; j += 32)
+                    if (gloc[j].y > 0.0) m = fmax(m, gloc[j].x);
+                m = warp_max(m);
+                double sm = 0.0;
+                for (int j = lane; j < nloc; j += 32)
+                    if (gloc[j].y > 0.0) sm += gloc[j].y * exp(gloc[j].x - m);
+                t = make_double2(m, warp_sum(sm));
+            } else {
+                double a1 = 0.0, a2 = 0.0;
+                for (int j = lane; j < nloc; j += 32) {
+                    a1 += gloc[j].x;
+                    a2 += gloc[j].y;
+                }
+                t = make_double2(warp_sum(a1), warp_sum(a2));
+            }
+            if (lane < CS) *cl.map_shared_rank(&rtot[rank], lane) = t;
+        }
+    }
     if (tr) trace(P, 8 * b + 4);
-    cl.sync();  // granule masses visible to rank 0 (and every DSMEM read of `part` is done)
+    cl.sync();  // rank totals delivered; granule masses visible in global memory
     if (tr) trace(P, 8 * b + 5);
     if (d.mode == MODE_NONE) return;
-    if (rank == 0)
-        for (int g = tid; g < P.NG; g += kClThreads) {
-            const int k = g / GPS, j = g - k * GPS;
-            gcache[g] = *cl.map_shared_rank(&gloc[j], k);
+    const double u = zg[2 * G + G];  // u_final (verify_reference.cpp:98)
+    // Every rank combines the totals in the same order: denominators
+    // (verify_reference.cpp:51-62 / dist.cpp:114-121 at slice resolution) and
+    // the rank whose slice holds u * denominator (the locator).
+    if (warp == 0) {
+        const double2 t = lane < CS ? rtot[lane] : make_double2(0.0, 0.0);
+        bool useA = false;
+        double denom = 1.0, gM = 0.0, gS = 1.0, w;
+        if (d.mode == MODE_REJECT) {
+            const double sa = warp_sum(t.x), sp = warp_sum(t.y);
+            useA = sa > kZeroEps;  // verify_reference.cpp:57-62
+            denom = useA ? sa : sp;
+            w = useA ? t.x : t.y;
+        } else if (ACT == ACT_SOFTMAX) {
+            gM = warp_max(lane < CS && t.y > 0.0 ? t.x : -CUDART_INF);
+            w = lane < CS && t.y > 0.0 ? t.y * exp(t.x - gM) : 0.0;
+            gS = warp_sum(w);
+        } else {
+            w = t.y;
+            denom = warp_sum(w);
         }
-    cl.sync();  // rank 0 is done reading the others' shared memory
-    if (rank != 0) return;
+        const double norm = d.mode != MODE_REJECT && ACT == ACT_SOFTMAX ? gS : denom;
+        const double incl = warp_scan_incl(w), run = incl - w;
+        const double thr = u * norm;
+        const unsigned hm = __ballot_sync(kFull, lane < CS && thr < run + w);
+        const int owner = hm ? __ffs(hm) - 1 : -1;
+        if (lane == 0) {
+            sh.loc_g = owner;
+            sh.loc_useA = useA;
+            sh.loc_d[0] = __shfl_sync(kFull, run, owner >= 0 ? owner : 0);
+            sh.loc_d[1] = denom;
+            sh.loc_d[2] = gM;
+            sh.loc_d[3] = gS;
+            if (rank == 0) {
+                if (P.rsu) P.rsu[b] = d.mode == MODE_REJECT ? 1 : 0;
+                if (P.rden) P.rden[b] = d.mode == MODE_REJECT && useA ? denom : 0.0;
+            }
+        } else {
+            (void)__shfl_sync(kFull, run, owner >= 0 ? owner : 0);
+        }
+    }
+    __syncthreads();
+    const int owner = sh.loc_g;
+    if (rank != (owner >= 0 ? owner : 0)) return;  // one locator per batch row
+    const bool tl = P.trace && b == 0 && tid == 0;  // locate stamps: trace[8B + 18 ..]
     if (tr) trace(P, 8 * b + 6);
-    locate<T, ACT, kClThreads>(P, b, d, sh, gcache, zg[2 * G + G], /*cached=*/true);
-    if (tr) {
-        trace(P, 8 * b + 7);
-        atomicMax(&P.trace[8 * P.B + 1], gtime());
+    if (tl) trace(P, 8 * P.B + 21);
+    RowCtx R;
+    R.mode = d.mode;
+    R.Mp = d.Mp;
+    R.Sp = d.Sp;
+    R.Mq = d.Mq;
+    R.Sq = d.Sq;
+    R.useA = sh.loc_useA;
+    R.denom = sh.loc_d[1];
+    const double gM = sh.loc_d[2], gS = sh.loc_d[3];
+    const bool soft_bonus = d.mode != MODE_REJECT && ACT == ACT_SOFTMAX;
+    if (soft_bonus) {
+        R.Mp = gM;
+        R.Sp = gS;
+        R.denom = 1.0;  // sample_row's sequential_sum of a softmax row (1 within rounding)
+    }
+    const double norm = soft_bonus ? gS : R.denom;
+    // granule level inside the locator's slice (warp 0): contiguous lane ranges,
+    // one warp scan, first granule whose prefix passes u * norm
+    if (warp == 0) {
+        int gst = -1;
+        double car = 0.0;
+        if (owner >= 0) {
+            auto wloc = [&](int j) -> double {  // unnormalized granule mass
+                const double2 v = gloc[j];
+                if (d.mode == MODE_REJECT) return R.useA ? v.x : v.y;
+                if (ACT == ACT_SOFTMAX) return v.y > 0.0 ? v.y * exp(v.x - gM) : 0.0;
+                return v.y;
+            };
+            const int gpl = (nloc + 31) / 32;
+            const int ja = min(nloc, lane * gpl), jb = min(nloc, ja + gpl);
+            double sm = 0.0;
+            for (int j = ja; j < jb; ++j) sm += wloc(j);
+            const double incl = warp_scan_incl(sm), tot = __shfl_sync(kFull, incl, 31);
+            double run = sh.loc_d[0] + (incl - sm);
+            const double thr = u * norm;
+            int hit = 0x7fffffff;
+            double hit_carry = 0.0;
+            for (int j = ja; j < jb; ++j) {
+                const double w = wloc(j);
+                if (thr < run + w) {
+                    hit = j;
+                    hit_carry = run / norm;
+                    break;
+                }
+                run += w;
+            }
+            const unsigned hm = __ballot_sync(kFull, hit != 0x7fffffff);
+            const int src = hm ? __ffs(hm) - 1 : 0;
+            const int jh = __shfl_sync(kFull, hit, src);
+            car = __shfl_sync(kFull, hit_carry, src);
+            if (hm) {
+                gst = rank * GPS + jh;
+            } else {  // rounding between the slice total and its granules: continue after the slice
+                gst = rank * GPS + nloc;
+                car = (sh.loc_d[0] + tot) / norm;
+            }
+        }
+        if (lane == 0) {
+            sh.loc_g = gst;
+            sh.loc_d[0] = car;
+        }
+    }
+    __syncthreads();
+    if (tl) trace(P, 8 * P.B + 18);
+    const double2* gp = P.gpart + (size_t)b * P.NG;
+    auto gmass = [&](int g) -> double {  // normalized granule mass (fallback path)
+        const double2 v = __ldcg(&gp[g]);
+        if (R.mode == MODE_REJECT) return (R.useA ? v.x : v.y) / R.denom;
+        if (ACT == ACT_SOFTMAX) return v.y > 0.0 ? v.y * exp(v.x - gM) / gS : 0.0;
+        return v.y / R.denom;
+    };
+    const T* pr = p_row<T>(P, b, d.row);
+    const T* qr = d.mode == MODE_REJECT ? q_row<T>(P, b, d.row) : nullptr;
+    const int token = locate_scan<T, ACT, kClThreads>(P, R, pr, qr, sh.loc_g, sh.loc_d[0], u, gmass, sh, tl);
+    if (tl) trace(P, 8 * P.B + 20);
+    if (tid == 0) {
+        P.fin[b] = token;
+        if (P.trace) {
+            trace(P, 8 * b + 7);
+            atomicMax(&P.trace[8 * P.B + 1], gtime());
+        }
     }
 }
 
@@ -1750,7 +1906,7 @@ constexpr int kClusterSmemTwoPerSm = 100 * 1024;  // two CTAs per SM (twice the 
 static int cluster_smem(const StepParams& P, int s, int NRc, int NS, int SE, int GPS) {
     const int VEC = 16 / s;
     const int RB = ((SE + 2 * VEC) * s + 15) & ~15;
-    long bytes = (long)NS * RB + 8L * ((NS + 1) & ~1) + 16L * (NRc + GPS + P.NG) + 8L * (3 * P.G + 1) + 8L * NS + 64;
+    long bytes = (long)NS * RB + 8L * ((NS + 1) & ~1) + 16L * (NRc + GPS + 16) + 8L * (3 * P.G + 1) + 8L * NS + 64;
     return bytes > kClusterSmemMax ? -1 : (int)bytes;
 }
 
@@ -1790,7 +1946,7 @@ template <typename T, int ACT>
 static bool plan_cluster_t(StepParams& P, int s) {
     static const bool off = getenv("SSV_NO_CLUSTER") != nullptr;  // experiment knob
     static const bool dbg = getenv("SSV_DEBUG") != nullptr;
-    if (off || P.sample_mode || P.G > 256 || P.NG > kLocCap) return false;
+    if (off || P.sample_mode || P.G > 256) return false;
     const int NRc = ACT == ACT_SOFTMAX ? 2 * P.G + (P.NR > 2 * P.G ? 1 : 0) : 0;  // bonus stats only if materialized
     if (NRc > kMaxRowsSmem) return false;  // the decision reads every row's statistics from SMEM
     // (two-CTA clusters measured slower than the streaming kernel at B = 64)

@@ -18,7 +18,7 @@ from dataclasses import dataclass
 import numpy as np
 
 PKG_DIR = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG_DIR, "libssv.so")
+LIB_PATH = os.environ.get("SSV_LIB") or os.path.join(PKG_DIR, "libssv.so")  # SSV_LIB: experiment builds only
 MAKEFILE = os.path.join(PKG_DIR, "csrc", "Makefile")
 
 SSV_OK, SSV_ECUDA, SSV_EINVAL = 0, 1, 2
