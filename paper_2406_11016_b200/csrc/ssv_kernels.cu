@@ -1258,14 +1258,19 @@ __global__ void __launch_bounds__(kClThreads, 1) k_verify_cluster(StepParams P) 
         bulk_g2s(slots + (size_t)sl * RB, reinterpret_cast<const void*>(s0), (uint32_t)(s1 - s0), &full[sl]);
     };
     const bool tx = tr && b == 0;  // finer stamps for batch row 0: trace[8B + 2 + k]
-    if (EXACT && tid == 0) {
-        for (int i = 0; i < NS; ++i) {
-            mbar_init(&full[i], 1);
-            fills[i] = 0;
+    if (EXACT && warp == 0) {
+        if (lane == 0) {
+            for (int i = 0; i < NS; ++i) {
+                mbar_init(&full[i], 1);
+                fills[i] = 0;
+            }
+            mbar_fence_init();
         }
-        mbar_fence_init();
+        __syncwarp();
+        // first fills, one row per lane: a bulk-copy issue costs ~250 cycles, so
+        // one thread issuing them all delays the last one by ~1 us
         if (n > 0)
-            for (int r = 0; r < NS; ++r) stage_row(r);
+            for (int r = lane; r < NS; r += 32) stage_row(r);
     }
     if (tx) trace(P, 8 * P.B + 2);
     // gathers and uniforms (needed by every rank for the decision)
