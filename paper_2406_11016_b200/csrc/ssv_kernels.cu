@@ -47,7 +47,7 @@ namespace ssv {
 
 constexpr int kMaxRowsSmem = 96;  // row statistics a decide keeps in SMEM (gamma <= 47)
 constexpr int kBG = 2;            // granules per warp per B-item (a B-item covers kBG * 4096 elements per row)
-constexpr int kCtaMinBlocks = 3;  // resident CTAs per SM (64 KB ring each)
+constexpr int kCtaMinBlocks = (227 * 1024) / (kDynSmem + 4096);  // resident CTAs per SM (3 with the 64 KB ring)
 static_assert(kLocCap * sizeof(double2) <= (size_t)kDynSmem, "granule cache aliases the ring");
 
 struct ItemRef {
@@ -310,13 +310,16 @@ struct AStream {
 };
 
 __device__ __forceinline__ void cp_async_wait_pending(unsigned n) {  // wait until <= n groups pending
+    static_assert(kAStages >= 2 && kAStages <= 8, "wait switch covers up to 7 pending groups");
     switch (n) {
         case 0: cp_async_wait<0>(); break;
         case 1: cp_async_wait<1>(); break;
         case 2: cp_async_wait<2>(); break;
-        default: cp_async_wait<3>(); break;
+        case 3: cp_async_wait<3>(); break;
+        case 4: cp_async_wait<4>(); break;
+        case 5: cp_async_wait<5>(); break;
+        default: cp_async_wait<6>(); break;
     }
-    static_assert(kAStages == 4, "wait switch covers kAStages - 1 pending groups");
 }
 
 // A-item: run q of statistics row r of batch row b.  The run's chunks stream
@@ -414,14 +417,17 @@ __device__ void item_A(const StepParams& P, int b, int idx, const ItemRef& nxt, 
             }
             if (m != -FLT_MAX) {  // a thread that has seen pads only contributes nothing
                 const float2 negM = make_float2(-m, -m);
-                float2 s0 = make_float2(0.f, 0.f), s1 = make_float2(0.f, 0.f);
 #pragma unroll
-                for (int j = 0; j < kAVec; ++j) {
-                    if (j & 1) AStat<T>::expsum(w[j], negM, s1);
-                    else AStat<T>::expsum(w[j], negM, s0);
+                for (int j0 = 0; j0 < kAVec; j0 += 4) {  // <= 16 fp32 terms per pair lane, then fp64
+                    float2 s0 = make_float2(0.f, 0.f), s1 = make_float2(0.f, 0.f);
+#pragma unroll
+                    for (int j = j0; j < j0 + 4 && j < kAVec; ++j) {
+                        if (j & 1) AStat<T>::expsum(w[j], negM, s1);
+                        else AStat<T>::expsum(w[j], negM, s0);
+                    }
+                    const float2 t = __fadd2_rn(s0, s1);
+                    s += (double)t.x + (double)t.y;
                 }
-                const float2 t = __fadd2_rn(s0, s1);  // <= 16 fp32 terms per pair lane, then fp64
-                s += (double)t.x + (double)t.y;
             }
         }
     }

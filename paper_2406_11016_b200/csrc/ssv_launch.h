@@ -18,7 +18,7 @@ constexpr bool is_sigmoid(int act) { return act == ACT_SIGMOID || act == ACT_SIG
 enum Mode : int { MODE_NONE = 0, MODE_REJECT = 1, MODE_BONUS = 2 };
 
 // Work-item geometry of k_verify (one CTA of kCtaThreads threads per item):
-//   A-item  a run of runA consecutive 16 KB chunks (16-byte aligned) of one
+//   A-item  a run of runA consecutive 32 KB chunks (16-byte aligned) of one
 //           statistics row, streamed through a kAStages-deep cp.async ring of
 //           per-thread shared-memory slots (kAVec 16-byte vectors per thread
 //           per chunk).
@@ -29,9 +29,15 @@ enum Mode : int { MODE_NONE = 0, MODE_REJECT = 1, MODE_BONUS = 2 };
 //   L-item  the inverse CDF (locate) of one batch row.
 constexpr int kCtaThreads = 256;
 constexpr int kWarpsPerCta = kCtaThreads / 32;
-constexpr int kAVec = 4;                                 // 16-byte vectors per thread per chunk
-constexpr int kAStages = 4;                              // cp.async ring depth
-constexpr int kAChunkBytes = kCtaThreads * kAVec * 16;   // 16 KB
+#ifndef SSV_AVEC
+#define SSV_AVEC 8
+#endif
+#ifndef SSV_ASTAGES
+#define SSV_ASTAGES 2
+#endif
+constexpr int kAVec = SSV_AVEC;                          // 16-byte vectors per thread per chunk
+constexpr int kAStages = SSV_ASTAGES;                    // cp.async ring depth
+constexpr int kAChunkBytes = kCtaThreads * kAVec * 16;   // 32 KB
 constexpr int kDynSmem = kAStages * kAChunkBytes;        // 64 KB (aliased by locate's granule cache)
 constexpr int kCB = 4096;
 constexpr int kGW = kCB / (kCtaThreads / 32);  // 512
@@ -52,7 +58,7 @@ struct StepParams {
     const double* u;
     int B, G, V, PS;   // batch, gamma, vocab, p steps (gamma or gamma+1)
     int NR;            // statistics rows per batch row (0: no A phase)
-    int Kc;            // 16 KB chunks per statistics row (any alignment)
+    int Kc;            // kAChunkBytes chunks per statistics row (any alignment)
     int runA;          // chunks per A-item
     int K;             // A-items (= partials) per statistics row
     int nA, nB;        // A- and B-items per batch row
