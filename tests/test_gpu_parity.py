@@ -455,3 +455,48 @@ def test_sigmoid_emulate_half(verifier, oracle, ref, mag):
         mism += int((~same).sum())
         assert np.all(np.abs(gn.residual_denom - o.residual_denom) <= 1e-6 * np.maximum(1, np.abs(o.residual_denom)))
     assert mism <= 1
+
+
+@pytest.mark.parametrize("path", ["streaming", "cluster"])
+def test_locate_edges(verifier, oracle, path):
+    """Inverse-CDF corner cases on both kernels (dist.cpp:122-137,
+    verify_reference.cpp:51-62): u_final at the largest double below 1 and at
+    0; a residual whose only mass is the row's first or last element (first /
+    last cluster rank's slice); the bonus row with a one-hot softmax.  fp32
+    probabilities: every row rejects at c = 0 (u = 0.999999 > tau)."""
+    rng = np.random.default_rng(21)
+    B, gamma, V = 6, 2, 51865
+    q = rng.random((B, gamma, V)) + 0.1
+    q /= q.sum(axis=2, keepdims=True)
+    p = q.copy()
+    p[0, 0, V - 1] += 1e-3  # residual only at the last element
+    p[1, 0, 0] += 1e-3      # ... only at the first element
+    p[2:, 0] = rng.random((B - 2, V)) + 0.1
+    p[2:, 0] /= p[2:, 0].sum(axis=1, keepdims=True)
+    p[:2, 0, 777] = 0.5 * q[:2, 0, 777]  # rows 0, 1 draft token 777: tau = 0.5, no residual there
+    p, q = oracle.round_f32(p), oracle.round_f32(q)
+    ids = rng.integers(0, V, (B, gamma)).astype(np.int32)
+    ids[:, 0] = np.argmin(p[:, 0] / q[:, 0], axis=1)  # tau well below 1 at c = 0
+    ids[:2, 0] = 777
+    u = np.full((B, gamma + 1), 0.999999)
+    u[:, gamma] = [0.5, 0.5, np.nextafter(1.0, 0.0), 0.0, 1e-300, 0.9999999]
+    verifier.set_path(path)
+    try:
+        o = oracle.verify_sequential(p, q, ids, u)
+        assert (o.accepted_len == 0).all()
+        assert o.final_token[0] == V - 1 and o.final_token[1] == 0
+        g = _run(verifier, "probs", *to_device(oracle, p, q, ids, u, "f32"))
+        assert compare(o, g, p, q, ids, u, "probs", label=f"{path}-locate") == 0
+        # bonus row: one-hot softmax (all mass on one logit) and a flat row
+        zp = oracle.round_f32(rng.normal(0, 1, (2, gamma + 1, V)))
+        zq = zp[:, :gamma].copy()
+        zp[0, gamma, 12345] = 200.0
+        ids2 = rng.integers(0, V, (2, gamma)).astype(np.int32)
+        u2 = np.zeros((2, gamma + 1))
+        u2[:, gamma] = [np.nextafter(1.0, 0.0), 0.3]
+        o = oracle.verify_exact(zp, zq, ids2, u2)
+        assert (o.accepted_len == gamma).all() and o.final_token[0] == 12345
+        g = _run(verifier, "exact", *to_device(oracle, zp, zq, ids2, u2, "f32"))
+        assert compare(o, g, zp, zq, ids2, u2, "exact", label=f"{path}-bonus") == 0
+    finally:
+        verifier.set_path("auto")
