@@ -1339,30 +1339,44 @@ __global__ void __launch_bounds__(kClThreads, 1) k_verify_cluster(StepParams P) 
                 };
                 const int vi1 = max(1, nv - 1);
                 float2 s0 = make_float2(0.f, 0.f), s1 = make_float2(0.f, 0.f);
-                auto step = [&](const uint4* w, int nw) {
+                float2 s2 = make_float2(0.f, 0.f), s3 = make_float2(0.f, 0.f);
+                auto step = [&](const uint4* w, int nw) {  // nw <= 9 vectors, four sum chains
                     float cm = -FLT_MAX;
 #pragma unroll
-                    for (int u = 0; u < 5; ++u)
+                    for (int u = 0; u < 9; ++u)
                         if (u < nw) AStat<T>::minmax(w[u], cm, mn);
                     if (cm > m) {
                         const float f = ex2f((m - cm) * 1.4426950408889634f);  // 0 on the first step
-                        s0 = __fmul2_rn(s0, make_float2(f, f));
-                        s1 = __fmul2_rn(s1, make_float2(f, f));
+                        const float2 ff = make_float2(f, f);
+                        s0 = __fmul2_rn(s0, ff);
+                        s1 = __fmul2_rn(s1, ff);
+                        s2 = __fmul2_rn(s2, ff);
+                        s3 = __fmul2_rn(s3, ff);
                         m = cm;
                     }
                     if (m != -FLT_MAX) {  // a lane that has seen pads only adds nothing
                         const float2 negM = make_float2(-m, -m);
 #pragma unroll
-                        for (int u = 0; u < 5; ++u)
-                            if (u < nw) AStat<T>::expsum(w[u], negM, (u & 1) ? s1 : s0);
+                        for (int u = 0; u < 9; ++u)
+                            if (u < nw) AStat<T>::expsum(w[u], negM, (u & 3) == 0 ? s0 : (u & 3) == 1 ? s1 : (u & 3) == 2 ? s2 : s3);
                     }
                 };
+                // Steps of eight vectors per lane (the per-step max / rescale
+                // latency amortized over twice the terms), then four, then the
+                // remainder with the two edge vectors.
                 int v0 = 1 + lane;
-                for (; v0 + 96 < vi1; v0 += 128) {
+                for (; v0 + 224 < vi1; v0 += 256) {
+                    uint4 w[8];
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) w[u] = rv[v0 + 32 * u];
+                    step(w, 8);
+                }
+                if (v0 + 96 < vi1) {
                     uint4 w[4];
 #pragma unroll
                     for (int u = 0; u < 4; ++u) w[u] = rv[v0 + 32 * u];
                     step(w, 4);
+                    v0 += 128;
                 }
                 {  // the remainder (< 4 vectors per lane) and the edge vectors
                     uint4 w[5];
@@ -1371,6 +1385,8 @@ __global__ void __launch_bounds__(kClThreads, 1) k_verify_cluster(StepParams P) 
                     w[4] = lane == 0 ? edge(0) : (lane == 1 && nv > 1 ? edge(nv - 1) : pad_vec<T>());
                     step(w, 5);
                 }
+                s0 = __fadd2_rn(s0, s2);
+                s1 = __fadd2_rn(s1, s3);
                 sd = ((double)s0.x + (double)s0.y) + ((double)s1.x + (double)s1.y);
                 __syncwarp();
                 if (txw && r < 6) trace(P, 8 * P.B + 12 + r);
@@ -1965,11 +1981,6 @@ static bool plan_cluster_t(StepParams& P, int s) {
         const int SE = ((P.V + cs - 1) / cs + kGW - 1) / kGW * kGW;
         const int GPS = SE / kGW;
         const int RB = NRc > 0 ? ((SE + 2 * (16 / s)) * s + 15) & ~15 : 0;
-        // Measured crossover vs the streaming kernel (tools/sweep.py, gamma 1-16 x
-        // B 1-64 x V 32000-151936): a CTA's slices of all rows must stay small
-        // enough for its shared-memory ring -- ~300 KB, ~520 KB at B >= 48
-        // where the streaming kernel's per-row tail costs more.
-        if ((long)NRc * RB > (P.B >= 48 ? 520L : 300L) * 1024) continue;
         // every row resident if that still leaves two CTAs per SM, else a ring
         int NS = NRc;
         const int all_rows = NS > 0 ? cluster_smem(P, s, NRc, NS, SE, GPS) : 0;  // -1: beyond one SM
@@ -1977,6 +1988,14 @@ static bool plan_cluster_t(StepParams& P, int s) {
             const int base = cluster_smem(P, s, NRc, 0, SE, GPS);
             NS = std::max(2, std::min(NRc, (kClusterSmemTwoPerSm - base) / std::max(RB + 20, 1)));
         }
+        // Measured crossover vs the streaming kernel (tools/sweep.py, gamma 1-16 x
+        // B 1-64 x V 32000-151936, fp32 / bf16): a CTA's slices of all its rows
+        // must stay small for its shared-memory ring -- up to ~300 KB; ~600 KB
+        // with a ring of >= 4 slots; ~520 KB at B >= 48, where the streaming
+        // kernel's per-row tail costs more.
+        const long cta_bytes = (long)NRc * RB;
+        if (!(cta_bytes <= 300L * 1024 || (NS >= 4 && cta_bytes <= 600L * 1024) || (P.B >= 48 && cta_bytes <= 520L * 1024)))
+            continue;
         const int smem = cluster_smem(P, s, NRc, NS, SE, GPS);
         if (smem < 0) continue;
         const int mac = max_active_clusters<T, ACT>(cs, smem);
