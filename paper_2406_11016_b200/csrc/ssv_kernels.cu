@@ -1,36 +1,36 @@
 // ssv_kernels.cu -- sm_100a kernels of the speculative-sampling verification step.
 //
-// k_verify<T, ACT> is the whole step in ONE launch of independent work items,
-// one 256-thread CTA each, ordered so every wait is on an item with a smaller
-// block index (DESIGN.md has the derivation and the roofline):
+// Two single-launch implementations of the whole step (DESIGN.md 3 has the
+// derivation and the roofline); the host picks one per call (plan_cluster):
 //
-//   A-item  (exact only) a 16-byte-aligned chunk of one drafted p / q row,
-//           4 KB * nv of it, loaded straight into registers with 128-bit
-//           streaming loads (nv loads in flight per thread).  CTA max with
-//           FMNMX3, then e^(x - max) with packed FADD2/FMUL2 + MUFU ex2 summed in
-//           fp32 pairs, fp64 across threads -> one partial (max, sum).
-//           The CTA that completes batch row b's LAST A-item folds the
-//           partials into row statistics, evaluates tau at every drafted
-//           position in fp64 (activation.cpp:20-27 + verify_reference.cpp:
-//           87-92), runs the first-rejection scan (93-96) and publishes the
-//           decision (release flag).
-//   B-item  kCB elements of the ONE row (bonus) or row PAIR (rejected
-//           position) batch row b still needs; each warp reduces one granule
-//           to its residual mass max(0, p - q) (or p mass / (m, s) for the
-//           bonus row).  Exact: the item waits for b's decision, which its
-//           position in the grid (after the A-items of b + lag) makes ready,
-//           and it re-reads the rejected pair from L2, not HBM.  Sigmoid /
-//           probabilities: the item takes the decision itself from the B*gamma
-//           gathered values (paper section 3.2.2) -- no row reductions, no wait.
-//           The CTA completing b's LAST B-item runs the inverse CDF: fp64
-//           granule prefix, then an exact fp64 scan inside the selected granule
-//           (dist.cpp:122-137, incl. its fallbacks), and resets b's counters.
+// k_verify<T, ACT> -- streaming path (any size; C4).  Persistent 256-thread
+// CTAs claim work items in order from a global counter; every wait is on an
+// item with a smaller claim index (held by a running CTA), so any grid size is
+// deadlock-free.  Items of batch row b:
+//   A-item  (exact only) a run of 32 KB chunks of one drafted p / q row through
+//           a 2-deep cp.async ring of per-thread 16-byte slots (no barrier);
+//           per thread a running max (FMNMX3 / packed bf16 max) and
+//           sum e^(x - max) (FADD2/FMUL2 + MUFU ex2 in fp32 pairs of <= 16
+//           terms, fp64 across); one fp64 partial per warp.  The next claimed
+//           run's first chunk streams while this run drains.
+//   D-item  exact: folds b's partials into row statistics, tau at every
+//           drafted position in fp64 (activation.cpp:20-27 +
+//           verify_reference.cpp:87-92), first rejection (93-96); sigmoid /
+//           probabilities: the decision from the B*gamma gathered values alone
+//           (paper section 3.2.2).  Publishes the decision (release flag).
+//   B-item  8192 elements of the ONE row (bonus) or row PAIR (rejected
+//           position) b still needs -> 512-element granule masses (L2-hot
+//           re-read of the rejected pair).
+//   L-item  inverse CDF: fp64 granule prefix, then the exact fp64 element scan
+//           (locate_scan; dist.cpp:122-137 incl. its fallbacks); resets b's
+//           counters.
 //
-// Items are dispatched in block-index order (the in-order CTA rasterization
-// single-pass scans rely on), so a waiting B-item's A-items are all resident
-// or retired: no deadlock, no persistent scheduler.  Every reduction has a
-// fixed topology, so results are bit-identical run to run.  k_materialize
-// (optional p / q / residual grids) and the synthetic-input generator follow.
+// k_verify_cluster<T, ACT> -- cluster path (batches whose rows each get a
+// co-resident thread-block cluster; C1-C3), described above the kernel.
+//
+// Every reduction has a fixed topology, so results are bit-identical run to
+// run.  k_materialize (optional p / q / residual grids) and the synthetic-input
+// generator follow.
 #include <algorithm>
 #include <cfloat>
 #include <cstdio>
@@ -1201,23 +1201,25 @@ __global__ void __launch_bounds__(kCtaThreads, kCtaMinBlocks) k_verify(StepParam
 }
 
 // ---------------------------------------------------------------------------
-// K1c/K2c k_verify_cluster<T, ACT>: the small-batch path.  One
-// thread-block cluster of cl_size CTAs per batch row; rank k owns the element
+// K1c/K2c k_verify_cluster<T, ACT>: the cluster path.  One
+// thread-block cluster of cl_size (16, 12, 8 or 4) CTAs per batch row; rank k owns the element
 // slice [k*SE, (k+1)*SE) of every row:
 //   1. exact: one TMA bulk copy per drafted p / q row stages the rank's slice of
 //      the row in a ring of cl_slots shared-memory slots (all rows at once when
 //      they fit), while all threads gather the drafted logits and the
 //      uniforms; one warp per row folds the slice to (max, sum e^(x - max)) as
-//      it lands (FMNMX3; fp32 pairs of <= 16 terms, fp64 across) and restages
+//      it lands (FMNMX3; four fp32 sum chains, fp64 in the folds) and restages
 //      the slot it consumed with a later row;
 //   2. cluster barrier; every CTA folds the cl_size slice partials of every row
 //      through DSMEM in the same fixed order, so all ranks reach the identical
 //      decision (tau in fp64, first rejection) without another exchange;
 //      sigmoid / probabilities: the decision comes from the gathers alone;
 //   3. each rank reduces its slice of the rejected pair / bonus row (L2-hot) to
-//      512-element granule masses;
-//   4. cluster barrier; rank 0 gathers the granule masses through DSMEM and runs
-//      the inverse CDF (locate).
+//      512-element granule masses and pushes its slice total into every rank's
+//      shared memory (DSMEM stores);
+//   4. cluster barrier; every rank combines the totals in the same order, and
+//      the rank whose slice holds u * denominator runs the inverse CDF over its
+//      own granules and elements (no DSMEM access after the barrier).
 constexpr int kClThreads = 256;  // cluster CTAs: 8 warps (512 measured slower at C2: two CTAs per SM halve the per-row bandwidth)
 constexpr int kClWarps = kClThreads / 32;
 
