@@ -1363,22 +1363,22 @@ __global__ void __launch_bounds__(kClThreads, 1) k_verify_cluster(StepParams P) 
                             if (u < nw) AStat<T>::expsum(w[u], negM, (u & 3) == 0 ? s0 : (u & 3) == 1 ? s1 : (u & 3) == 2 ? s2 : s3);
                     }
                 };
-                // Steps of eight vectors per lane (the per-step max / rescale
-                // latency amortized over twice the terms), then four, then the
-                // remainder with the two edge vectors.
+                // fp32: steps of eight vectors per lane (the per-step max /
+                // rescale latency amortized over twice the terms; bf16 vectors
+                // already hold eight terms), then four, then the remainder with
+                // the two edge vectors.
                 int v0 = 1 + lane;
-                for (; v0 + 224 < vi1; v0 += 256) {
+                for (; sizeof(T) == 4 && v0 + 224 < vi1; v0 += 256) {
                     uint4 w[8];
 #pragma unroll
                     for (int u = 0; u < 8; ++u) w[u] = rv[v0 + 32 * u];
                     step(w, 8);
                 }
-                if (v0 + 96 < vi1) {
+                for (; v0 + 96 < vi1; v0 += 128) {
                     uint4 w[4];
 #pragma unroll
                     for (int u = 0; u < 4; ++u) w[u] = rv[v0 + 32 * u];
                     step(w, 4);
-                    v0 += 128;
                 }
                 {  // the remainder (< 4 vectors per lane) and the edge vectors
                     uint4 w[5];

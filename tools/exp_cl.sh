@@ -1,7 +1,5 @@
 #!/bin/bash
 OUT=gpurun_out; mkdir -p $OUT
-S=""
-for V in 32000 51865 151936; do for g in 1 4 8 16; do for B in 1 4 16 32 64; do S="$S $B,$g,$V,f32"; done; done; done
-timeout 900 python tools/sweep.py exact $S > $OUT/sw_cl.txt 2>&1
-SSV_NO_CLUSTER=1 timeout 900 python tools/sweep.py exact $S > $OUT/sw_st.txt 2>&1
+timeout 600 python -m pytest tests -m gpu -q --timeout 120 > $OUT/pytest_gpu.txt 2>&1; echo "pytest rc=$?" >> $OUT/pytest_gpu.txt
+for i in 1 2; do python tools/sweep.py exact 1,5,32000,f32 8,5,51865,f32 64,8,32000,f32 64,8,32000,bf16 8,8,51865,bf16; done > $OUT/exp_sweep.txt 2>&1
 echo done
