@@ -1090,10 +1090,20 @@ template <typename T, int ACT>
 __device__ void item_B(const StepParams& P, int b, int j, Shared& sh) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     if (j == 0 && tid == 0) trace(P, 8 * b + 3);
+    const int g0 = j * kWarps * kBG;
+    // Sigmoid / probabilities (no A phase): while the row's gathers-only
+    // decision is pending, pull this item's slice of the bonus row into L2 --
+    // the likely case (high acceptance); a rejection reads the pair instead.
+    if (ACT != ACT_SOFTMAX && !P.sample_mode && P.PS == P.G + 1) {
+        const size_t e0 = (size_t)g0 * kGW, e1 = min((size_t)P.V, e0 + (size_t)kWarps * kBG * kGW);
+        const char* row = reinterpret_cast<const char*>(p_row<T>(P, b, P.G));
+        const size_t lo = (e0 * sizeof(T)) & ~size_t(127), hi = e1 * sizeof(T);
+        const size_t at = lo + (size_t)tid * 128;
+        if (at < hi) asm volatile("prefetch.global.L2 [%0];" ::"l"(row + at));
+    }
     get_decision<T, ACT>(P, b, false, sh);
     if (j == 0 && tid == 0) trace(P, 8 * b + 4);
     const Decision d = sh.dec;
-    const int g0 = j * kWarps * kBG;
     if (d.mode != MODE_NONE) {
         GranuleData<T> D[kBG];
 #pragma unroll
