@@ -1230,11 +1230,14 @@ __global__ void __launch_bounds__(kCtaThreads, kCtaMinBlocks) k_verify(StepParam
 //   4. cluster barrier; every rank combines the totals in the same order, and
 //      the rank whose slice holds u * denominator runs the inverse CDF over its
 //      own granules and elements (no DSMEM access after the barrier).
-constexpr int kClThreads = 256;  // cluster CTAs: 8 warps (512 measured slower at C2: two CTAs per SM halve the per-row bandwidth)
-constexpr int kClWarps = kClThreads / 32;
+// Cluster CTAs: 8 warps, or 16 when one CTA per SM keeps every row slice
+// resident and the rows outnumber 8 warps (one warp per row: no second round
+// of row folds on the critical path; plan_cluster_t).
+constexpr int kClThreads = 256;
 
-template <typename T, int ACT>
-__global__ void __launch_bounds__(kClThreads, 1) k_verify_cluster(StepParams P) {
+template <typename T, int ACT, int NT = kClThreads>
+__global__ void __launch_bounds__(NT, 1) k_verify_cluster(StepParams P) {
+    constexpr int kClWarps = NT / 32;
     namespace cg = cooperative_groups;
     constexpr int VEC = Elem<T>::VEC;
     constexpr bool EXACT = ACT == ACT_SOFTMAX;
@@ -1292,7 +1295,7 @@ __global__ void __launch_bounds__(kClThreads, 1) k_verify_cluster(StepParams P) 
     }
     if (tx) trace(P, 8 * P.B + 2);
     // gathers and uniforms (needed by every rank for the decision)
-    for (int c = tid; c < G; c += kClThreads) {
+    for (int c = tid; c < G; c += NT) {
         int x = P.ids[(size_t)b * G + c];
         if (x < 0 || x >= V) {
             if (rank == 0) flag(P, SSV_STATUS_TOKEN_RANGE);
@@ -1301,7 +1304,7 @@ __global__ void __launch_bounds__(kClThreads, 1) k_verify_cluster(StepParams P) 
         zg[c] = load_exact(p_row<T>(P, b, c) + x);
         zg[G + c] = load_exact(q_row<T>(P, b, c) + x);
     }
-    for (int c = tid; c <= G; c += kClThreads) {
+    for (int c = tid; c <= G; c += NT) {
         const double u = P.u[(size_t)b * (G + 1) + c];
         zg[2 * G + c] = u;
         if (rank == 0 && P.check_uniforms && (!(u >= 0.0) || !(u < 1.0))) flag(P, SSV_STATUS_UNIFORM_RANGE);
@@ -1662,7 +1665,7 @@ __global__ void __launch_bounds__(kClThreads, 1) k_verify_cluster(StepParams P) 
     };
     const T* pr = p_row<T>(P, b, d.row);
     const T* qr = d.mode == MODE_REJECT ? q_row<T>(P, b, d.row) : nullptr;
-    const int token = locate_scan<T, ACT, kClThreads>(P, R, pr, qr, sh.loc_g, sh.loc_d[0], u, gmass, sh, tl);
+    const int token = locate_scan<T, ACT, NT>(P, R, pr, qr, sh.loc_g, sh.loc_d[0], u, gmass, sh, tl);
     if (tl) trace(P, 8 * P.B + 20);
     if (tid == 0) {
         P.fin[b] = token;
@@ -1949,16 +1952,21 @@ static int cluster_smem(const StepParams& P, int s, int NRc, int NS, int SE, int
     return bytes > kClusterSmemMax ? -1 : (int)bytes;
 }
 
-template <typename T, int ACT>
+template <typename T, int ACT, int NT>
 static int max_active_clusters(int cs, int smem) {
-    static int cached_cs = -1, cached_smem = -1, cached = 0;
-    if (cs == cached_cs && smem == cached_smem) return cached;
-    auto k = k_verify_cluster<T, ACT>;
+    struct Entry {
+        int cs, smem, n;
+    };
+    static Entry cache[16];  // the plans a serving loop alternates between
+    static int n_cached = 0, next = 0;
+    for (int i = 0; i < n_cached; ++i)
+        if (cache[i].cs == cs && cache[i].smem == smem) return cache[i].n;
+    auto k = k_verify_cluster<T, ACT, NT>;
     cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, kClusterSmemMax);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(cs, 1, 1);
-    cfg.blockDim = dim3(kClThreads, 1, 1);
+    cfg.blockDim = dim3(NT, 1, 1);
     cfg.dynamicSmemBytes = smem;
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeClusterDimension;
@@ -1972,9 +1980,9 @@ static int max_active_clusters(int cs, int smem) {
         cudaGetLastError();
         n = 0;
     }
-    cached_cs = cs;
-    cached_smem = smem;
-    cached = n;
+    cache[next] = Entry{cs, smem, n};
+    next = (next + 1) % 16;
+    n_cached = n_cached < 16 ? n_cached + 1 : 16;
     return n;
 }
 
@@ -1989,10 +1997,47 @@ static bool plan_cluster_t(StepParams& P, int s) {
     const int NRc = ACT == ACT_SOFTMAX ? 2 * P.G + (P.NR > 2 * P.G ? 1 : 0) : 0;  // bonus stats only if materialized
     if (NRc > kMaxRowsSmem) return false;  // the decision reads every row's statistics from SMEM
     // (two-CTA clusters measured slower than the streaming kernel at B = 64)
-    for (int cs : {16, 12, 8, 4}) {
+    static const int res_mode = getenv("SSV_RES_MODE") ? atoi(getenv("SSV_RES_MODE")) : 2;  // experiment knob
+    static const int force_cs = getenv("SSV_FORCE_CS") ? atoi(getenv("SSV_FORCE_CS")) : 0;  // experiment knob
+    for (int pass = res_mode == 2 ? 0 : 1; pass < 2; ++pass)
+    for (int cs : {16, 12, 11, 10, 9, 8, 4}) {
+        if (force_cs && cs != force_cs) continue;
+        if (pass == 1 && cs > 8 && cs < 12) continue;  // odd sizes only for the resident plan
+        const bool no_resident = res_mode == 0 || (res_mode == 2 && pass == 1);
         const int SE = ((P.V + cs - 1) / cs + kGW - 1) / kGW * kGW;
         const int GPS = SE / kGW;
         const int RB = NRc > 0 ? ((SE + 2 * (16 / s)) * s + 15) & ~15 : 0;
+        // Small batches first try one CTA per SM with every row slice resident
+        // (no ring restaging on the critical path), 16 warps when the rows
+        // outnumber 8 (one row fold per warp); used only if all B clusters
+        // are still co-resident.
+        if constexpr (ACT == ACT_SOFTMAX) {
+          if (!no_resident && (long)P.B * cs <= sm_count()) {
+            const int smem1 = cluster_smem(P, s, NRc, NRc, SE, GPS);
+            if (smem1 > kClusterSmemTwoPerSm) {
+                const int nt = NRc > 8 ? 512 : 256;
+                const int mac = nt == 512 ? max_active_clusters<T, ACT, 512>(cs, smem1)
+                                          : max_active_clusters<T, ACT, 256>(cs, smem1);
+                if (dbg)
+                    fprintf(stderr, "ssv: cluster plan (resident) act=%d B=%d V=%d rows=%d cs=%d SE=%d smem=%d threads=%d max_active=%d\n",
+                            ACT, P.B, P.V, NRc, cs, SE, smem1, nt, mac);
+                if (mac >= P.B) {
+                    P.cl_size = cs;
+                    P.cl_se = SE;
+                    P.cl_gps = GPS;
+                    P.cl_rows = NRc;
+                    P.cl_slots = NRc;
+                    P.cl_rowbytes = RB;
+                    P.cl_smem = smem1;
+                    P.cl_threads = nt;
+                    P.dbg = 0;
+                    P.NR = NRc;
+                    return true;
+                }
+            }
+          }
+        }
+        if (pass == 0) continue;
         // every row resident if that still leaves two CTAs per SM, else a ring
         int NS = NRc;
         const int all_rows = NS > 0 ? cluster_smem(P, s, NRc, NS, SE, GPS) : 0;  // -1: beyond one SM
@@ -2010,7 +2055,7 @@ static bool plan_cluster_t(StepParams& P, int s) {
             continue;
         const int smem = cluster_smem(P, s, NRc, NS, SE, GPS);
         if (smem < 0) continue;
-        const int mac = max_active_clusters<T, ACT>(cs, smem);
+        const int mac = max_active_clusters<T, ACT, kClThreads>(cs, smem);
         if (dbg)
             fprintf(stderr, "ssv: cluster plan act=%d B=%d V=%d rows=%d slots=%d cs=%d SE=%d smem=%d max_active=%d\n",
                     ACT, P.B, P.V, NRc, NS, cs, SE, smem, mac);
@@ -2022,6 +2067,7 @@ static bool plan_cluster_t(StepParams& P, int s) {
         P.cl_slots = NS;
         P.cl_rowbytes = RB;
         P.cl_smem = smem;
+        P.cl_threads = kClThreads;
         static const int dbgm = getenv("SSV_DBG_MODE") ? atoi(getenv("SSV_DBG_MODE")) : 0;
         P.dbg = dbgm;
         if (ACT == ACT_SOFTMAX) P.NR = NRc;  // rowstat rows the cluster path writes
@@ -2051,7 +2097,7 @@ template <typename T, int ACT>
 static void launch_cluster_t(const StepParams& P, const Launch& L) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)(P.B * P.cl_size), 1, 1);
-    cfg.blockDim = dim3(kClThreads, 1, 1);
+    cfg.blockDim = dim3((unsigned)P.cl_threads, 1, 1);
     cfg.dynamicSmemBytes = P.cl_smem;
     cfg.stream = L.st;
     cudaLaunchAttribute at[2];
@@ -2062,6 +2108,13 @@ static void launch_cluster_t(const StepParams& P, const Launch& L) {
     cfg.attrs = at;
     cfg.numAttrs = 1 + pdl_attr(at[1]);
     const int h = L.begin(KID_VERIFY);
+    if constexpr (ACT == ACT_SOFTMAX) {
+        if (P.cl_threads == 512) {
+            cudaLaunchKernelEx(&cfg, k_verify_cluster<T, ACT, 512>, P);
+            L.end(h);
+            return;
+        }
+    }
     cudaLaunchKernelEx(&cfg, k_verify_cluster<T, ACT>, P);
     L.end(h);
 }

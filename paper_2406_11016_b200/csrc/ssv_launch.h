@@ -75,6 +75,7 @@ struct StepParams {
     // CTAs per batch row, rank k stages elements [k*cl_se, (k+1)*cl_se) of every
     // row it needs in its shared memory.
     int cl_size, cl_se, cl_gps, cl_rows, cl_slots, cl_rowbytes, cl_smem;
+    int cl_threads;  // 256, or 512 for all-resident slices with more rows than 8 warps
     int dbg;  // experiment bits (SSV_DBG_MODE), 0 in production
     double alpha, width;
     int sample_mode;     // sample softmax(z_p row b) with u[b] (draft sampling)
