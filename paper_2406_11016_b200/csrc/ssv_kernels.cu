@@ -672,12 +672,26 @@ __device__ __forceinline__ double exact_act(const StepParams& P, double z, doubl
 
 // Value the inverse CDF scans at element i (fp64): residual max(0, p - q)
 // (verify_reference.cpp:51-55) or the p row itself (fallback / bonus).
+// A shared-memory copy of elements [lo, hi) of the p and q rows (cluster path,
+// every row slice resident): p[i - lo], q[i - lo]; hi = 0 when there is none.
+template <typename T>
+struct RowSlice {
+    const T* p = nullptr;
+    const T* q = nullptr;
+    int lo = 0, hi = 0;
+};
+
+template <typename T>
+__device__ __forceinline__ double row_elem(const T* g, const T* s, const RowSlice<T>& S, int i) {
+    return i >= S.lo && i < S.hi ? (double)load_smem_elem(s + (i - S.lo)) : load_exact(g + i);
+}
+
 template <typename T, int ACT>
 __device__ __forceinline__ double exact_value(const StepParams& P, const RowCtx& R, const T* pr, const T* qr,
-                                              int i) {
-    const double p = exact_act<ACT>(P, load_exact(pr + i), R.Mp, R.Sp);
+                                              int i, const RowSlice<T>& S = RowSlice<T>()) {
+    const double p = exact_act<ACT>(P, row_elem(pr, S.p, S, i), R.Mp, R.Sp);
     if (R.mode == MODE_REJECT && R.useA) {
-        const double q = exact_act<ACT>(P, load_exact(qr + i), R.Mq, R.Sq);
+        const double q = exact_act<ACT>(P, row_elem(qr, S.q, S, i), R.Mq, R.Sq);
         const double d = p - q;
         return d > 0.0 ? d : 0.0;
     }
@@ -698,15 +712,18 @@ struct GranuleData {
     int n;
 };
 
-template <typename T>
-__device__ __forceinline__ void granule_load(const StepParams& P, int b, int g, const Decision& d, GranuleData<T>& D) {
+// SM: sp / sq point at the granule's first element in shared memory (the
+// cluster path's resident slices) instead of the rows in global memory.
+template <typename T, bool SM = false>
+__device__ __forceinline__ void granule_load(const StepParams& P, int b, int g, const Decision& d, GranuleData<T>& D,
+                                             const T* sp = nullptr, const T* sq = nullptr) {
     using A = typename Elem<T>::acc;
     const int lane = threadIdx.x & 31;
     const int lo = g * kGW;
     D.n = g < P.NG ? min(kGW, P.V - lo) : 0;
     const bool reject = d.mode == MODE_REJECT;
-    const T* pr = p_row<T>(P, b, d.row) + lo;
-    const T* qr = reject ? q_row<T>(P, b, d.row) + lo : pr;
+    const T* pr = SM ? sp : p_row<T>(P, b, d.row) + lo;
+    const T* qr = SM ? sq : (reject ? q_row<T>(P, b, d.row) + lo : pr);
     constexpr int EPL = GranuleData<T>::EPL;
     if constexpr (sizeof(T) == 2) {
         // bf16, full granule of 16-byte-aligned rows: each lane takes 16
@@ -721,8 +738,8 @@ __device__ __forceinline__ void granule_load(const StepParams& P, int b, int g, 
             uint4 wp[NV], wq[NV];
 #pragma unroll
             for (int k = 0; k < NV; ++k) {
-                wp[k] = __ldg(vp + k);
-                if (reject) wq[k] = __ldg(vq + k);
+                wp[k] = SM ? vp[k] : __ldg(vp + k);
+                if (reject) wq[k] = SM ? vq[k] : __ldg(vq + k);
             }
             constexpr int VEC = Elem<T>::VEC;
 #pragma unroll
@@ -742,8 +759,8 @@ __device__ __forceinline__ void granule_load(const StepParams& P, int b, int g, 
 #pragma unroll
     for (int t = 0; t < EPL; ++t) {
         const int e = t * 32 + lane;
-        D.xs[t] = e < D.n ? load_elem(pr + e) : (A)0;
-        D.xq[t] = (reject && e < D.n) ? load_elem(qr + e) : (A)0;
+        D.xs[t] = e < D.n ? (SM ? load_smem_elem(pr + e) : load_elem(pr + e)) : (A)0;
+        D.xq[t] = (reject && e < D.n) ? (SM ? load_smem_elem(qr + e) : load_elem(qr + e)) : (A)0;
     }
 }
 
@@ -847,7 +864,7 @@ __device__ void granule(const StepParams& P, int b, int g, const Decision& d, do
 // else 0), with gmass(g) the normalized mass of granule g.  Returns the token.
 template <typename T, int ACT, int NT, typename GMass>
 __device__ int locate_scan(const StepParams& P, const RowCtx& R, const T* pr, const T* qr, int gstar, double carry,
-                           double u, const GMass& gmass, Shared& sh, bool tl) {
+                           double u, const GMass& gmass, Shared& sh, bool tl, const RowSlice<T>& S = RowSlice<T>()) {
     const int NG = P.NG, GW = kGW;
     int token = -1;
     constexpr int E = (kGW + NT - 1) / NT;  // elements per thread (2 at 256 threads, 1 at 512)
@@ -857,8 +874,8 @@ __device__ int locate_scan(const StepParams& P, const RowCtx& R, const T* pr, co
         const int hi = min(lo + GW, P.V);
         const int base = lo + threadIdx.x * E;
         double v0 = 0.0, v1 = 0.0;
-        if (base < hi) v0 = exact_value<T, ACT>(P, R, pr, qr, base) / R.denom;
-        if (E > 1 && base + 1 < hi) v1 = exact_value<T, ACT>(P, R, pr, qr, base + 1) / R.denom;
+        if (base < hi) v0 = exact_value<T, ACT>(P, R, pr, qr, base, S) / R.denom;
+        if (E > 1 && base + 1 < hi) v1 = exact_value<T, ACT>(P, R, pr, qr, base + 1, S) / R.denom;
         const double ts = v0 + v1;
         if (tl) trace(P, 8 * P.B + 19);
         double tot;
@@ -1278,6 +1295,20 @@ __global__ void __launch_bounds__(NT, 1) k_verify_cluster(StepParams P) {
         mbar_arrive_expect_tx(&full[sl], (uint32_t)(s1 - s0));
         bulk_g2s(slots + (size_t)sl * RB, reinterpret_cast<const void*>(s0), (uint32_t)(s1 - s0), &full[sl]);
     };
+    // This rank's slice of the bonus row (16-byte superset), pulled into L2
+    // ahead of a possible bonus sample: the sigmoid / probabilities decision
+    // needs only the gathers (likely bonus); exact waits until its slices have
+    // landed (resident plan only -- a ring still streams) so the prefetch does
+    // not compete with them.
+    auto prefetch_bonus = [&]() {
+        const T* row = p_row<T>(P, b, G);
+        const uintptr_t a0 = reinterpret_cast<uintptr_t>(row + e0), a1 = reinterpret_cast<uintptr_t>(row + e0 + n);
+        const uintptr_t s0 = a0 & ~uintptr_t(15), s1 = (a1 + 15) & ~uintptr_t(15);
+        bulk_prefetch_l2(reinterpret_cast<const void*>(s0), (uint32_t)(s1 - s0));
+    };
+    const bool want_bonus_pf = P.PS == G + 1 && n > 0 && !(P.dbg & 4) &&
+                               (EXACT ? (NS == NRc && NRc == 2 * G) : true);
+    if (!EXACT && want_bonus_pf && tid == 0) prefetch_bonus();
     const bool tx = tr && b == 0;  // finer stamps for batch row 0: trace[8B + 2 + k]
     if (EXACT && warp == 0) {
         if (lane == 0) {
@@ -1334,6 +1365,7 @@ __global__ void __launch_bounds__(NT, 1) k_verify_cluster(StepParams P) {
                     __syncwarp();
                 }
                 mbar_wait(&full[sl], (unsigned)(r / NS) & 1u);
+                if (r == NRc - 1 && want_bonus_pf && lane == 0) prefetch_bonus();  // last slice landed
                 const bool txw = P.trace && rank == 0 && b == 0 && lane == 0;
                 if (txw && r < 8) trace(P, 8 * P.B + 4 + r);
                 const int off = offs[sl], nv = (off + n + VEC - 1) / VEC;
@@ -1508,11 +1540,29 @@ __global__ void __launch_bounds__(NT, 1) k_verify_cluster(StepParams P) {
     // total (fixed order) is pushed into every rank's rtot[rank] so that after
     // the barrier each rank holds all totals locally (no DSMEM reads after it).
     const int nloc = max(0, min(GPS, P.NG - rank * GPS));  // this rank's granules
+    // Every row slice resident (exact): the rejected pair's slices are still in
+    // this rank's shared memory -- granules and the element scan read them there.
+    RowSlice<T> rs;
+    if (EXACT && NS == NRc && d.mode == MODE_REJECT && n > 0) {
+        const int sp = d.row, sq = G + d.row;
+        rs.p = reinterpret_cast<const T*>(slots + (size_t)sp * RB) + offs[sp];
+        rs.q = reinterpret_cast<const T*>(slots + (size_t)sq * RB) + offs[sq];
+        rs.lo = e0;
+        rs.hi = e0 + n;
+    }
     if (d.mode != MODE_NONE) {
         for (int j = warp; j < GPS; j += kClWarps) {
             const int g = rank * GPS + j;
             double2 out = make_double2(0.0, 0.0);
-            if (g < P.NG) granule<T, ACT>(P, b, g, d, &out);
+            if (g < P.NG) {
+                if (rs.hi > 0) {
+                    GranuleData<T> D;
+                    granule_load<T, true>(P, b, g, d, D, rs.p + (g * kGW - e0), rs.q + (g * kGW - e0));
+                    out = granule_reduce<T, ACT>(P, d, D);
+                } else {
+                    granule<T, ACT>(P, b, g, d, &out);
+                }
+            }
             if (lane == 0) {
                 gloc[j] = out;
                 if (g < P.NG) P.gpart[(size_t)b * P.NG + g] = out;
@@ -1665,7 +1715,7 @@ __global__ void __launch_bounds__(NT, 1) k_verify_cluster(StepParams P) {
     };
     const T* pr = p_row<T>(P, b, d.row);
     const T* qr = d.mode == MODE_REJECT ? q_row<T>(P, b, d.row) : nullptr;
-    const int token = locate_scan<T, ACT, NT>(P, R, pr, qr, sh.loc_g, sh.loc_d[0], u, gmass, sh, tl);
+    const int token = locate_scan<T, ACT, NT>(P, R, pr, qr, sh.loc_g, sh.loc_d[0], u, gmass, sh, tl, rs);
     if (tl) trace(P, 8 * P.B + 20);
     if (tid == 0) {
         P.fin[b] = token;
@@ -2030,7 +2080,8 @@ static bool plan_cluster_t(StepParams& P, int s) {
                     P.cl_rowbytes = RB;
                     P.cl_smem = smem1;
                     P.cl_threads = nt;
-                    P.dbg = 0;
+                    static const int dbgm = getenv("SSV_DBG_MODE") ? atoi(getenv("SSV_DBG_MODE")) : 0;
+                    P.dbg = dbgm;  // experiment bits (4: no bonus-row prefetch)
                     P.NR = NRc;
                     return true;
                 }

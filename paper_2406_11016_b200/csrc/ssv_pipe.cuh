@@ -54,6 +54,12 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
         : "memory");
 }
 
+// Pull [src, src + bytes) into L2 without a destination (16-byte aligned
+// address, size % 16 == 0).
+__device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
+
 // Named barrier 1 over the consumer warps only (the producer warp never joins).
 template <int N>
 __device__ __forceinline__ void cbar() {
