@@ -106,6 +106,7 @@ int ssv_last_launch_count(const ssv_ctx* ctx);
 #define SSV_PATH_AUTO 0
 #define SSV_PATH_STREAMING 1
 #define SSV_PATH_CLUSTER 2 /* falls back to streaming where the cluster kernel cannot run */
+#define SSV_PATH_CLUSTER_RING 3 /* cluster kernel, two-CTAs-per-SM ring plan only (no resident plan) */
 int ssv_set_path(ssv_ctx* ctx, int32_t path);
 const char* ssv_version(void);
 

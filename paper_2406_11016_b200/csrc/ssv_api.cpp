@@ -184,7 +184,7 @@ int run_device(ssv_ctx* ctx, int variant, const ssv_verify_args* a, ssv_verify_o
     P.emulate_half = variant == V_SIGMOID && (a->flags & SSV_EMULATE_HALF) ? 1 : 0;
     const int act = P.emulate_half ? ACT_SIGMOID_HALF : variant;  // the emulation has its own kernels
     plan_geometry(a->dtype, act, P);
-    if (ctx->path != SSV_PATH_STREAMING) plan_cluster(a->dtype, act, P);
+    if (ctx->path != SSV_PATH_STREAMING) plan_cluster(a->dtype, act, P, ctx->path != SSV_PATH_CLUSTER_RING);
     const Layout L = plan_scratch(P, 0);
     rc = ensure_scratch(ctx, L.total, (size_t)P.B);
     if (rc) return rc;
@@ -401,7 +401,7 @@ int ssv_last_launch_count(const ssv_ctx* ctx) { return ctx ? ctx->launches : 0; 
 
 int ssv_set_path(ssv_ctx* ctx, int32_t path) {
     if (!ctx) return SSV_EINVAL;
-    if (path != SSV_PATH_AUTO && path != SSV_PATH_STREAMING && path != SSV_PATH_CLUSTER)
+    if (path != SSV_PATH_AUTO && path != SSV_PATH_STREAMING && path != SSV_PATH_CLUSTER && path != SSV_PATH_CLUSTER_RING)
         return fail(ctx, SSV_EINVAL, "ssv_set_path: unknown path %d", path);
     ctx->path = path;
     return SSV_OK;

@@ -2040,14 +2040,15 @@ static int max_active_clusters(int cs, int smem) {
 // Largest cluster (most SMs per row) whose slices fit in shared memory and of
 // which B fit on the GPU together.
 template <typename T, int ACT>
-static bool plan_cluster_t(StepParams& P, int s) {
+static bool plan_cluster_t(StepParams& P, int s, bool allow_resident) {
     static const bool off = getenv("SSV_NO_CLUSTER") != nullptr;  // experiment knob
     static const bool dbg = getenv("SSV_DEBUG") != nullptr;
     if (off || P.sample_mode || P.G > 256) return false;
     const int NRc = ACT == ACT_SOFTMAX ? 2 * P.G + (P.NR > 2 * P.G ? 1 : 0) : 0;  // bonus stats only if materialized
     if (NRc > kMaxRowsSmem) return false;  // the decision reads every row's statistics from SMEM
     // (two-CTA clusters measured slower than the streaming kernel at B = 64)
-    static const int res_mode = getenv("SSV_RES_MODE") ? atoi(getenv("SSV_RES_MODE")) : 2;  // experiment knob
+    static const int res_env = getenv("SSV_RES_MODE") ? atoi(getenv("SSV_RES_MODE")) : 2;  // experiment knob
+    const int res_mode = allow_resident ? res_env : 0;
     static const int force_cs = getenv("SSV_FORCE_CS") ? atoi(getenv("SSV_FORCE_CS")) : 0;  // experiment knob
     for (int pass = res_mode == 2 ? 0 : 1; pass < 2; ++pass)
     for (int cs : {16, 12, 11, 10, 9, 8, 4}) {
@@ -2127,19 +2128,19 @@ static bool plan_cluster_t(StepParams& P, int s) {
     return false;
 }
 
-bool plan_cluster(int dtype, int act, StepParams& P) {
+bool plan_cluster(int dtype, int act, StepParams& P, bool allow_resident) {
     P.cl_size = 0;
     if (dtype == DT_F32) {
-        if (act == ACT_SOFTMAX) return plan_cluster_t<float, ACT_SOFTMAX>(P, 4);
-        if (act == ACT_SIGMOID) return plan_cluster_t<float, ACT_SIGMOID>(P, 4);
-        if (act == ACT_SIGMOID_HALF) return plan_cluster_t<float, ACT_SIGMOID_HALF>(P, 4);
-        return plan_cluster_t<float, ACT_PROBS>(P, 4);
+        if (act == ACT_SOFTMAX) return plan_cluster_t<float, ACT_SOFTMAX>(P, 4, allow_resident);
+        if (act == ACT_SIGMOID) return plan_cluster_t<float, ACT_SIGMOID>(P, 4, allow_resident);
+        if (act == ACT_SIGMOID_HALF) return plan_cluster_t<float, ACT_SIGMOID_HALF>(P, 4, allow_resident);
+        return plan_cluster_t<float, ACT_PROBS>(P, 4, allow_resident);
     }
     if (dtype == DT_BF16) {
-        if (act == ACT_SOFTMAX) return plan_cluster_t<__nv_bfloat16, ACT_SOFTMAX>(P, 2);
-        if (act == ACT_SIGMOID) return plan_cluster_t<__nv_bfloat16, ACT_SIGMOID>(P, 2);
-        if (act == ACT_SIGMOID_HALF) return plan_cluster_t<__nv_bfloat16, ACT_SIGMOID_HALF>(P, 2);
-        return plan_cluster_t<__nv_bfloat16, ACT_PROBS>(P, 2);
+        if (act == ACT_SOFTMAX) return plan_cluster_t<__nv_bfloat16, ACT_SOFTMAX>(P, 2, allow_resident);
+        if (act == ACT_SIGMOID) return plan_cluster_t<__nv_bfloat16, ACT_SIGMOID>(P, 2, allow_resident);
+        if (act == ACT_SIGMOID_HALF) return plan_cluster_t<__nv_bfloat16, ACT_SIGMOID_HALF>(P, 2, allow_resident);
+        return plan_cluster_t<__nv_bfloat16, ACT_PROBS>(P, 2, allow_resident);
     }
     return false;
 }

@@ -133,7 +133,7 @@ struct Launch {
 };
 
 void plan_geometry(int dtype, int act, StepParams& P);
-bool plan_cluster(int dtype, int act, StepParams& P);  // small-batch cluster path (sets cl_*)
+bool plan_cluster(int dtype, int act, StepParams& P, bool allow_resident = true);  // small-batch cluster path (sets cl_*)
 int trace_slots(const StepParams& P);
 void launch_verify(int dtype, int act, const StepParams& P, void* outp, void* outq, void* outr,
                    const Launch& L);

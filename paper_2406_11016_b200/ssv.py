@@ -202,8 +202,9 @@ class Verifier:
             self.lib.ssv_set_stream(self.ctx, C.c_void_p(torch.cuda.current_stream(self.device).cuda_stream))
 
     def set_path(self, path: str) -> None:
-        """Kernel selection: "auto" (default), "streaming" or "cluster" (ssv_set_path)."""
-        code = {"auto": 0, "streaming": 1, "cluster": 2}[path]
+        """Kernel selection (ssv_set_path): "auto" (default), "streaming", "cluster"
+        or "cluster_ring" (the cluster kernel without its resident plan)."""
+        code = {"auto": 0, "streaming": 1, "cluster": 2, "cluster_ring": 3}[path]
         self._check(self.lib.ssv_set_path(self.ctx, code), "ssv_set_path")
 
     @property
