@@ -501,3 +501,40 @@ def test_locate_edges(verifier, oracle, path):
         assert compare(o, g, zp, zq, ids2, u2, "exact", label=f"{path}-bonus") == 0
     finally:
         verifier.set_path("auto")
+
+
+@pytest.mark.parametrize("path", ["streaming", "cluster", "cluster_ring"])
+def test_locate_edges_exact_logits(verifier, oracle, path):
+    """The residual corner cases of test_locate_edges with fp32 LOGITS on the C2
+    shape (B=8, gamma=5, V=51865 -- the resident cluster plan, which scans the
+    rejected pair from shared memory): one draft logit raised at a single
+    element makes max(0, p - q) positive only there -- the row's first / last
+    element, and either side of the 10-CTA cluster's slice boundary (5632)
+    and of a granule boundary; u_final at the largest double below 1 and at 0
+    (verify_reference.cpp:51-62, dist.cpp:122-137)."""
+    rng = np.random.default_rng(22)
+    B, gamma, V = 8, 5, 51865
+    zq = rng.normal(0.0, 1.0, (B, gamma, V))
+    zp = np.concatenate([zq, rng.normal(0.0, 1.0, (B, 1, V))], axis=1)
+    spots = [V - 1, 0, 5631, 5632, 512 * 37 - 1, 512 * 37, V - 2, 1]
+    for b, j in enumerate(spots):
+        zp[b, 0, j] += 9.0
+    zp, zq = oracle.round_f32(zp), oracle.round_f32(zq)
+    ids = rng.integers(0, V, (B, gamma)).astype(np.int32)
+    for b, j in enumerate(spots):
+        ids[b, 0] = (j + 1000) % V  # tau = p/q < 1 away from the bump
+    u = np.full((B, gamma + 1), 0.999999)
+    u[:, gamma] = [0.5, 0.5, np.nextafter(1.0, 0.0), 0.0, 0.25, 0.75, 1e-300, 0.9999999]
+    o = oracle.verify_exact(zp, zq, ids, u)
+    assert (o.accepted_len == 0).all()
+    assert [int(t) for t in o.final_token] == spots
+    verifier.set_path(path)
+    try:
+        g = _run(verifier, "exact", *to_device(oracle, zp, zq, ids, u, "f32"))
+        assert compare(o, g, zp, zq, ids, u, "exact", label=f"{path}-exact-locate") == 0
+        gb = _run(verifier, "exact", *to_device(oracle, oracle.round_bf16(zp), oracle.round_bf16(zq), ids, u, "bf16"))
+        ob = oracle.verify_exact(oracle.round_bf16(zp), oracle.round_bf16(zq), ids, u)
+        zpb, zqb = oracle.round_bf16(zp), oracle.round_bf16(zq)
+        assert compare(ob, gb, zpb, zqb, ids, u, "exact", label=f"{path}-bf16-locate") == 0
+    finally:
+        verifier.set_path("auto")
