@@ -1,9 +1,8 @@
 #!/bin/bash
-# One-CTA-per-SM big-ring cluster plan (SSV_RING1) vs the default plans.
+# Resident plan also for slices that fit two CTAs per SM (padded to one per SM: SSV_RES_PAD).
 set -u
 OUT=gpurun_out; mkdir -p $OUT
-SH="64,8,32000,f32 64,8,32000,bf16 32,8,32000,f32 48,8,32000,f32 64,5,32000,f32 64,4,32000,f32 32,16,32000,f32 16,8,51865,f32 64,8,51865,f32 16,8,151936,f32 32,5,51865,f32 16,16,32000,f32"
-timeout 300 python tools/sweep.py exact $SH > $OUT/r1_0.txt 2>&1
-SSV_RING1=1 SSV_DEBUG=1 timeout 300 python tools/sweep.py exact $SH > $OUT/r1_1.txt 2>&1
-SSV_RING1=1 SSV_FORCE_CS=2 timeout 300 python tools/sweep.py exact $SH > $OUT/r1_cs2.txt 2>&1
-SSV_RING1=1 timeout 60 python tools/trace_step.py --B 64 --gamma 8 --V 32000 --dtype f32 --variant exact > $OUT/trace_c3.txt 2>&1
+SH="1,5,32000,f32 1,5,32000,bf16 1,2,32000,f32 2,5,32000,f32 4,5,32000,f32 8,5,32000,f32 8,8,32000,f32 8,5,51865,bf16 4,4,51865,f32 8,2,51865,f32 8,1,151936,f32 16,2,32000,f32 12,4,32000,f32 1,8,51865,f32 4,16,32000,bf16"
+timeout 300 python tools/sweep.py exact $SH > $OUT/p0.txt 2>&1
+SSV_RES_PAD=1 SSV_DEBUG=1 timeout 300 python tools/sweep.py exact $SH > $OUT/p1.txt 2>&1
+timeout 300 python tools/sweep.py exact $SH > $OUT/p0b.txt 2>&1
