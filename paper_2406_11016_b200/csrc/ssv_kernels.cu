@@ -1251,6 +1251,11 @@ __global__ void __launch_bounds__(kCtaThreads, kCtaMinBlocks) k_verify(StepParam
 // resident and the rows outnumber 8 warps (one warp per row: no second round
 // of row folds on the critical path; plan_cluster_t).
 constexpr int kClThreads = 256;
+// Rows x cluster ranks up to which every rank pushes its slice partials into
+// every rank's shared memory before the barrier (the fold after it then reads
+// only local shared memory); beyond it the fold reads the owners' partials
+// through DSMEM.
+constexpr int kClPushMax = 256;
 
 template <typename T, int ACT, int NT = kClThreads>
 __global__ void __launch_bounds__(NT, 1) k_verify_cluster(StepParams P) {
@@ -1274,13 +1279,18 @@ __global__ void __launch_bounds__(NT, 1) k_verify_cluster(StepParams P) {
     uint8_t* slots = csm;                                                       // NS x RB
     const int NSp = (NS + 1) & ~1;
     uint64_t* full = reinterpret_cast<uint64_t*>(slots + (size_t)NS * RB);      // NS (even-padded)
-    double2* part = reinterpret_cast<double2*>(full + NSp);                     // [NRc] slice partials (DSMEM)
-    double2* gloc = part + NRc;                                                 // [GPS] granule partials (DSMEM)
+    const int PM = NRc * CS <= kClPushMax ? CS : 1;                             // pushed partials per row
+    double2* part = reinterpret_cast<double2*>(full + NSp);                     // [NRc][PM] slice partials
+    double2* gloc = part + NRc * PM;                                            // [GPS] granule partials (DSMEM)
     double2* rtot = gloc + GPS;                                                 // [16] slice totals (pushed by the ranks)
     double* zg = reinterpret_cast<double*>(rtot + 16);                          // [3G + 1] gathers, uniforms
     int* offs = reinterpret_cast<int*>(zg + 3 * G + 1);                         // [NS]
     int* fills = offs + NS;                                                     // [NS] fills issued per slot - 1
 
+    // Every rank pushes its slice partials into the other ranks' shared memory
+    // before the first full cluster barrier: arrive now, wait (all ranks have
+    // started) just before the row folds.
+    if (EXACT) asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
     const bool tr = P.trace && rank == 0 && tid == 0;  // per-row stamps (tools/trace_step.py)
     if (tr) {
         trace(P, 8 * b);
@@ -1350,6 +1360,7 @@ __global__ void __launch_bounds__(NT, 1) k_verify_cluster(StepParams P) {
         // on one row at a time, rows in ring order -- ~1.5x slower at C1/C2:
         // the per-row warp folds then sit on the critical path.)
         float mn = FLT_MAX;
+        asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
         for (int r = warp; r < NRc; r += kClWarps) {
             const int sl = r % NS;
             float m = -FLT_MAX;
@@ -1446,9 +1457,12 @@ __global__ void __launch_bounds__(NT, 1) k_verify_cluster(StepParams P) {
             const float M = warp_max(m);
             double S = sd != 0.0 ? sd * exp((double)m - (double)M) : sd;  // NaN propagates
             S = warp_sum(S);
-            if (lane == 0) {
-                if (isnan(S) || M == INFINITY) flag(P, SSV_STATUS_NONFINITE);
-                part[r] = S != 0.0 ? make_double2((double)M, S) : make_double2(-CUDART_INF, 0.0);
+            const double2 pv = S != 0.0 ? make_double2((double)M, S) : make_double2(-CUDART_INF, 0.0);
+            if (lane == 0 && (isnan(S) || M == INFINITY)) flag(P, SSV_STATUS_NONFINITE);
+            if (PM > 1) {
+                if (lane < CS) *cl.map_shared_rank(&part[r * PM + rank], lane) = pv;
+            } else if (lane == 0) {
+                part[r] = pv;
             }
         }
         if (__any_sync(kFull, isinf(mn)) && lane == 0) flag(P, SSV_STATUS_NONFINITE);
@@ -1461,7 +1475,7 @@ __global__ void __launch_bounds__(NT, 1) k_verify_cluster(StepParams P) {
         for (int r0 = 2 * warp; r0 < NRc; r0 += 2 * kClWarps) {
             const int r = r0 + half;
             double2 v = make_double2(-CUDART_INF, 0.0);
-            if (r < NRc && hl < CS) v = *cl.map_shared_rank(&part[r], hl);
+            if (r < NRc && hl < CS) v = PM > 1 ? part[r * PM + hl] : *cl.map_shared_rank(&part[r], hl);
             double M = v.x;
 #pragma unroll
             for (int o = 8; o > 0; o >>= 1) M = fmax(M, __shfl_xor_sync(kFull, M, o, 16));
@@ -1995,10 +2009,11 @@ constexpr int kClusterSmemMax = 227 * 1024 - 4096;  // dynamic budget (static Sh
 
 constexpr int kClusterSmemTwoPerSm = 100 * 1024;  // two CTAs per SM (twice the resident clusters)
 
-static int cluster_smem(const StepParams& P, int s, int NRc, int NS, int SE, int GPS) {
+static int cluster_smem(const StepParams& P, int s, int NRc, int NS, int SE, int GPS, int cs) {
     const int VEC = 16 / s;
     const int RB = ((SE + 2 * VEC) * s + 15) & ~15;
-    long bytes = (long)NS * RB + 8L * ((NS + 1) & ~1) + 16L * (NRc + GPS + 16) + 8L * (3 * P.G + 1) + 8L * NS + 64;
+    const int PM = NRc * cs <= kClPushMax ? cs : 1;  // slice partials pushed to every rank
+    long bytes = (long)NS * RB + 8L * ((NS + 1) & ~1) + 16L * (NRc * PM + GPS + 16) + 8L * (3 * P.G + 1) + 8L * NS + 64;
     return bytes > kClusterSmemMax ? -1 : (int)bytes;
 }
 
@@ -2065,7 +2080,7 @@ static bool plan_cluster_t(StepParams& P, int s, bool allow_resident) {
         // are still co-resident.
         if constexpr (ACT == ACT_SOFTMAX) {
           if (!no_resident && (long)P.B * cs <= sm_count()) {
-            int smem1 = cluster_smem(P, s, NRc, NRc, SE, GPS);
+            int smem1 = cluster_smem(P, s, NRc, NRc, SE, GPS, cs);
             // Slices that would fit two CTAs per SM: padded to one CTA per SM
             // (C1 bf16 17.7 -> 14.8 us, B=1 gamma=2 16.4 -> 13.4 us).
             if (!res_nopad && smem1 >= 0 && smem1 <= kClusterSmemTwoPerSm) smem1 = kClusterSmemTwoPerSm + 16 * 1024;
@@ -2096,9 +2111,9 @@ static bool plan_cluster_t(StepParams& P, int s, bool allow_resident) {
         if (pass == 0) continue;
         // every row resident if that still leaves two CTAs per SM, else a ring
         int NS = NRc;
-        const int all_rows = NS > 0 ? cluster_smem(P, s, NRc, NS, SE, GPS) : 0;  // -1: beyond one SM
+        const int all_rows = NS > 0 ? cluster_smem(P, s, NRc, NS, SE, GPS, cs) : 0;  // -1: beyond one SM
         if (all_rows < 0 || all_rows > kClusterSmemTwoPerSm) {
-            const int base = cluster_smem(P, s, NRc, 0, SE, GPS);
+            const int base = cluster_smem(P, s, NRc, 0, SE, GPS, cs);
             NS = std::max(2, std::min(NRc, (kClusterSmemTwoPerSm - base) / std::max(RB + 20, 1)));
         }
         // Measured crossover vs the streaming kernel (tools/sweep.py, gamma 1-16 x
@@ -2109,7 +2124,7 @@ static bool plan_cluster_t(StepParams& P, int s, bool allow_resident) {
         const long cta_bytes = (long)NRc * RB;
         if (!(cta_bytes <= 300L * 1024 || (NS >= 4 && cta_bytes <= 600L * 1024) || (P.B >= 48 && cta_bytes <= 520L * 1024)))
             continue;
-        const int smem = cluster_smem(P, s, NRc, NS, SE, GPS);
+        const int smem = cluster_smem(P, s, NRc, NS, SE, GPS, cs);
         if (smem < 0) continue;
         const int mac = max_active_clusters<T, ACT, kClThreads>(cs, smem);
         if (dbg)
