@@ -1275,6 +1275,9 @@ __global__ void __launch_bounds__(NT, 1) k_verify_cluster(StepParams P) {
     const int e0 = min(V, rank * SE), n = min(V, e0 + SE) - e0;  // this rank's slice
     const int NRc = EXACT ? P.cl_rows : 0;
     const int NS = EXACT ? P.cl_slots : 1;  // ring slots (NS == NRc: every row resident at once)
+    // Ring units: each row slice in H pieces of PE elements (H == 1: whole slices)
+    const int H = EXACT ? P.cl_pieces : 1, PE = H > 1 ? P.cl_pe : SE, NU = NRc * H;
+    const bool whole = H == 1;
     // shared-memory carve-up (host: cluster_smem)
     uint8_t* slots = csm;                                                       // NS x RB
     const int NSp = (NS + 1) & ~1;
@@ -1296,10 +1299,17 @@ __global__ void __launch_bounds__(NT, 1) k_verify_cluster(StepParams P) {
         trace(P, 8 * b);
         if (b == 0) trace(P, 8 * P.B);
     }
-    auto stage_row = [&](int r) {  // thread 0: bulk-copy the 16-byte superset of row r's slice into slot r % NS
-        const int sl = r % NS;
+    auto piece_n = [&](int h) { return max(0, min(n, (h + 1) * PE) - h * PE); };  // elements of piece h
+    auto stage_row = [&](int u) {  // one thread: bulk-copy the 16-byte superset of unit u (row u / H, piece u % H) into slot u % NS
+        const int sl = u % NS, r = u / H, h = u % H;
         const T* row = r < G ? p_row<T>(P, b, r) : (r < 2 * G ? q_row<T>(P, b, r - G) : p_row<T>(P, b, G));
-        const uintptr_t a0 = reinterpret_cast<uintptr_t>(row + e0), a1 = reinterpret_cast<uintptr_t>(row + e0 + n);
+        const int pn = piece_n(h);
+        if (pn == 0) {  // nothing of this piece in the slice: complete the phase without a copy
+            offs[sl] = 0;
+            mbar_arrive(&full[sl]);
+            return;
+        }
+        const uintptr_t a0 = reinterpret_cast<uintptr_t>(row + e0 + h * PE), a1 = a0 + (uintptr_t)pn * sizeof(T);
         const uintptr_t s0 = a0 & ~uintptr_t(15), s1 = (a1 + 15) & ~uintptr_t(15);
         offs[sl] = (int)((a0 - s0) / sizeof(T));
         mbar_arrive_expect_tx(&full[sl], (uint32_t)(s1 - s0));
@@ -1317,7 +1327,7 @@ __global__ void __launch_bounds__(NT, 1) k_verify_cluster(StepParams P) {
         bulk_prefetch_l2(reinterpret_cast<const void*>(s0), (uint32_t)(s1 - s0));
     };
     const bool want_bonus_pf = P.PS == G + 1 && n > 0 && !(P.dbg & 4) &&
-                               (EXACT ? (NS == NRc && NRc == 2 * G) : true);
+                               (EXACT ? (whole && NS == NRc && NRc == 2 * G) : true);
     if (!EXACT && want_bonus_pf && tid == 0) prefetch_bonus();
     const bool tx = tr && b == 0;  // finer stamps for batch row 0: trace[8B + 2 + k]
     if (EXACT && warp == 0) {
@@ -1332,7 +1342,7 @@ __global__ void __launch_bounds__(NT, 1) k_verify_cluster(StepParams P) {
         // first fills, one row per lane: a bulk-copy issue costs ~250 cycles, so
         // one thread issuing them all delays the last one by ~1 us
         if (n > 0)
-            for (int r = lane; r < NS; r += 32) stage_row(r);
+            for (int u = lane; u < NS; u += 32) stage_row(u);
     }
     if (tx) trace(P, 8 * P.B + 2);
     // gathers and uniforms (needed by every rank for the decision)
@@ -1362,24 +1372,34 @@ __global__ void __launch_bounds__(NT, 1) k_verify_cluster(StepParams P) {
         float mn = FLT_MAX;
         asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
         for (int r = warp; r < NRc; r += kClWarps) {
-            const int sl = r % NS;
             float m = -FLT_MAX;
             double sd = 0.0;
-            if (n > 0) {
-                // Slot reuse: row r is the (r / NS)-th fill of its slot.  Parity
+            float2 s0 = make_float2(0.f, 0.f), s1 = make_float2(0.f, 0.f);
+            float2 s2 = make_float2(0.f, 0.f), s3 = make_float2(0.f, 0.f);
+            for (int h = 0; h < H && n > 0; ++h) {
+                const int u = r * H + h, sl = u % NS, pn = piece_n(h);
+                // Slot reuse: unit u is the (u / NS)-th fill of its slot.  Parity
                 // waits only tell the current phase from the one before, so first
-                // make sure the slot's previous row has been consumed (and row r
+                // make sure the slot's previous unit has been consumed (and unit u
                 // issued) -- a fresh barrier would otherwise pass a parity-1 wait.
-                if (r >= NS) {
+                if (u >= NS) {
                     if (lane == 0)
-                        while (ld_volatile_s32(&fills[sl]) < r / NS) __nanosleep(20);
+                        while (ld_volatile_s32(&fills[sl]) < u / NS) __nanosleep(20);
                     __syncwarp();
                 }
-                mbar_wait(&full[sl], (unsigned)(r / NS) & 1u);
-                if (r == NRc - 1 && want_bonus_pf && lane == 0) prefetch_bonus();  // last slice landed
-                const bool txw = P.trace && rank == 0 && b == 0 && lane == 0;
+                mbar_wait(&full[sl], (unsigned)(u / NS) & 1u);
+                if (u == NU - 1 && want_bonus_pf && lane == 0) prefetch_bonus();  // last slice landed
+                const bool txw = P.trace && rank == 0 && b == 0 && lane == 0 && h == 0;
                 if (txw && r < 8) trace(P, 8 * P.B + 4 + r);
-                const int off = offs[sl], nv = (off + n + VEC - 1) / VEC;
+                if (pn == 0) {  // (no copy was issued; the slot is free again)
+                    __syncwarp();
+                    if (lane == 0 && u + NS < NU) {
+                        stage_row(u + NS);
+                        st_volatile_s32(&fills[sl], (u + NS) / NS);
+                    }
+                    continue;
+                }
+                const int off = offs[sl], nv = (off + pn + VEC - 1) / VEC;
                 const uint4* rv = reinterpret_cast<const uint4*>(slots + (size_t)sl * RB);
                 // A step loads 4 vectors per lane (unguarded in the interior, so
                 // the 4 shared-memory loads are in flight together), takes their
@@ -1392,12 +1412,10 @@ __global__ void __launch_bounds__(NT, 1) k_verify_cluster(StepParams P) {
                 auto edge = [&](int v) {
                     uint4 w = rv[v];
                     if (v == 0 && off) mask_vec<T>(w, off, VEC);
-                    if (v == nv - 1 && (off + n) % VEC) mask_vec<T>(w, 0, (off + n) % VEC);
+                    if (v == nv - 1 && (off + pn) % VEC) mask_vec<T>(w, 0, (off + pn) % VEC);
                     return w;
                 };
                 const int vi1 = max(1, nv - 1);
-                float2 s0 = make_float2(0.f, 0.f), s1 = make_float2(0.f, 0.f);
-                float2 s2 = make_float2(0.f, 0.f), s3 = make_float2(0.f, 0.f);
                 auto step = [&](const uint4* w, int nw) {  // nw <= 9 vectors, four sum chains
                     float cm = -FLT_MAX;
 #pragma unroll
@@ -1443,15 +1461,16 @@ __global__ void __launch_bounds__(NT, 1) k_verify_cluster(StepParams P) {
                     w[4] = lane == 0 ? edge(0) : (lane == 1 && nv > 1 ? edge(nv - 1) : pad_vec<T>());
                     step(w, 5);
                 }
-                s0 = __fadd2_rn(s0, s2);
-                s1 = __fadd2_rn(s1, s3);
-                sd = ((double)s0.x + (double)s0.y) + ((double)s1.x + (double)s1.y);
                 __syncwarp();
                 if (txw && r < 6) trace(P, 8 * P.B + 12 + r);
-                if (lane == 0 && r + NS < NRc) {  // this warp was the slot's only reader
-                    stage_row(r + NS);
-                    st_volatile_s32(&fills[sl], (r + NS) / NS);  // row r + NS is in flight
+                if (lane == 0 && u + NS < NU) {  // this warp was the slot's only reader
+                    stage_row(u + NS);
+                    st_volatile_s32(&fills[sl], (u + NS) / NS);  // unit u + NS is in flight
                 }
+            }
+            {
+                const float2 a = __fadd2_rn(s0, s2), c = __fadd2_rn(s1, s3);
+                sd = ((double)a.x + (double)a.y) + ((double)c.x + (double)c.y);
             }
             // fold the lanes: M = max, S = sum of s_l e^(m_l - M) (fp64)
             const float M = warp_max(m);
@@ -1557,7 +1576,7 @@ __global__ void __launch_bounds__(NT, 1) k_verify_cluster(StepParams P) {
     // Every row slice resident (exact): the rejected pair's slices are still in
     // this rank's shared memory -- granules and the element scan read them there.
     RowSlice<T> rs;
-    if (EXACT && NS == NRc && d.mode == MODE_REJECT && n > 0) {
+    if (EXACT && whole && NS == NRc && d.mode == MODE_REJECT && n > 0) {
         const int sp = d.row, sq = G + d.row;
         rs.p = reinterpret_cast<const T*>(slots + (size_t)sp * RB) + offs[sp];
         rs.q = reinterpret_cast<const T*>(slots + (size_t)sq * RB) + offs[sq];
@@ -2009,9 +2028,9 @@ constexpr int kClusterSmemMax = 227 * 1024 - 4096;  // dynamic budget (static Sh
 
 constexpr int kClusterSmemTwoPerSm = 100 * 1024;  // two CTAs per SM (twice the resident clusters)
 
-static int cluster_smem(const StepParams& P, int s, int NRc, int NS, int SE, int GPS, int cs) {
+static int cluster_smem(const StepParams& P, int s, int NRc, int NS, int SE, int GPS, int cs, int PE = 0) {
     const int VEC = 16 / s;
-    const int RB = ((SE + 2 * VEC) * s + 15) & ~15;
+    const int RB = (((PE ? PE : SE) + 2 * VEC) * s + 15) & ~15;
     const int PM = NRc * cs <= kClPushMax ? cs : 1;  // slice partials pushed to every rank
     long bytes = (long)NS * RB + 8L * ((NS + 1) & ~1) + 16L * (NRc * PM + GPS + 16) + 8L * (3 * P.G + 1) + 8L * NS + 64;
     return bytes > kClusterSmemMax ? -1 : (int)bytes;
@@ -2100,6 +2119,8 @@ static bool plan_cluster_t(StepParams& P, int s, bool allow_resident) {
                     P.cl_rowbytes = RB;
                     P.cl_smem = smem1;
                     P.cl_threads = nt;
+                    P.cl_pieces = 1;
+                    P.cl_pe = SE;
                     static const int dbgm = getenv("SSV_DBG_MODE") ? atoi(getenv("SSV_DBG_MODE")) : 0;
                     P.dbg = dbgm;  // experiment bits (4: no bonus-row prefetch)
                     P.NR = NRc;
@@ -2124,21 +2145,38 @@ static bool plan_cluster_t(StepParams& P, int s, bool allow_resident) {
         const long cta_bytes = (long)NRc * RB;
         if (!(cta_bytes <= 300L * 1024 || (NS >= 4 && cta_bytes <= 600L * 1024) || (P.B >= 48 && cta_bytes <= 520L * 1024)))
             continue;
-        const int smem = cluster_smem(P, s, NRc, NS, SE, GPS, cs);
+        // A true ring streams pieces of the slices (H per slice, >= 16 KB each):
+        // a slot is refilled after a piece's fold, not a whole slice's
+        // (C3 f32, 32 KB slices in 16 KB pieces: 48.4 -> 44.7 us; 8 KB pieces
+        // measured slower than whole 16 KB slices).
+        static const int pieces_env = getenv("SSV_PIECES") ? atoi(getenv("SSV_PIECES")) : 0;  // experiment knob
+        int H = 1, PE = SE, NSu = NS;
+        const int want_h = pieces_env > 0 ? pieces_env : std::max(1, std::min(4, SE * s / 16384));
+        if (NS < NRc && want_h > 1) {
+            H = want_h;
+            PE = ((SE + H - 1) / H + kGW - 1) / kGW * kGW;
+            H = (SE + PE - 1) / PE;
+            const int RBp = ((PE + 2 * (16 / s)) * s + 15) & ~15;
+            const int base = cluster_smem(P, s, NRc, 0, SE, GPS, cs, PE);
+            NSu = std::max(2, std::min(NRc * H, (kClusterSmemTwoPerSm - base) / std::max(RBp + 20, 1)));
+        }
+        const int smem = cluster_smem(P, s, NRc, NSu, SE, GPS, cs, PE);
         if (smem < 0) continue;
         const int mac = max_active_clusters<T, ACT, kClThreads>(cs, smem);
         if (dbg)
-            fprintf(stderr, "ssv: cluster plan act=%d B=%d V=%d rows=%d slots=%d cs=%d SE=%d smem=%d max_active=%d\n",
-                    ACT, P.B, P.V, NRc, NS, cs, SE, smem, mac);
+            fprintf(stderr, "ssv: cluster plan act=%d B=%d V=%d rows=%d slots=%d pieces=%d cs=%d SE=%d smem=%d max_active=%d\n",
+                    ACT, P.B, P.V, NRc, NSu, H, cs, SE, smem, mac);
         if (mac < P.B) continue;
         P.cl_size = cs;
         P.cl_se = SE;
         P.cl_gps = GPS;
         P.cl_rows = NRc;
-        P.cl_slots = NS;
-        P.cl_rowbytes = RB;
+        P.cl_slots = NSu;
+        P.cl_rowbytes = H > 1 ? (((PE + 2 * (16 / s)) * s + 15) & ~15) : RB;
         P.cl_smem = smem;
         P.cl_threads = kClThreads;
+        P.cl_pieces = H;
+        P.cl_pe = PE;
         static const int dbgm = getenv("SSV_DBG_MODE") ? atoi(getenv("SSV_DBG_MODE")) : 0;
         P.dbg = dbgm;
         if (ACT == ACT_SOFTMAX) P.NR = NRc;  // rowstat rows the cluster path writes
