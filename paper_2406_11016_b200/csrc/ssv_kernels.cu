@@ -2143,7 +2143,14 @@ static bool plan_cluster_t(StepParams& P, int s, bool allow_resident) {
         // with a ring of >= 4 slots; ~520 KB at B >= 48, where the streaming
         // kernel's per-row tail costs more.
         const long cta_bytes = (long)NRc * RB;
-        if (!(cta_bytes <= 300L * 1024 || (NS >= 4 && cta_bytes <= 600L * 1024) || (P.B >= 48 && cta_bytes <= 520L * 1024)))
+        // Since the pieced ring (below): also up to 600 KB at B >= 32 and V <= 64K when
+        // the ring holds >= 3 slices or streams pieces (B=64 gamma=5 V=51865:
+        // 59.5 -> 53.8 us; B=32 gamma=8 V=51865: 52.3 -> 44.4 us; the V = 151936
+        // shapes stay on the streaming kernel, 6-60 % faster there).
+        const bool pieced = NS < NRc && SE * s >= 32768;
+        static const bool no_gate = getenv("SSV_NO_GATE") != nullptr;  // experiment knob
+        if (!no_gate && !(cta_bytes <= 300L * 1024 || (NS >= 4 && cta_bytes <= 600L * 1024) || (P.B >= 48 && cta_bytes <= 520L * 1024) ||
+                          (P.B >= 32 && P.V <= 65536 && cta_bytes <= 600L * 1024 && (NS >= 3 || pieced))))
             continue;
         // A true ring streams pieces of the slices (H per slice, >= 16 KB each):
         // a slot is refilled after a piece's fold, not a whole slice's
