@@ -2147,18 +2147,21 @@ static bool plan_cluster_t(StepParams& P, int s, bool allow_resident) {
         // the ring holds >= 3 slices or streams pieces (B=64 gamma=5 V=51865:
         // 59.5 -> 53.8 us; B=32 gamma=8 V=51865: 52.3 -> 44.4 us; the V = 151936
         // shapes stay on the streaming kernel, 6-60 % faster there).
-        const bool pieced = NS < NRc && SE * s >= 32768;
+        // pieces of >= 12 KB (measured: 12 KB beats 16 KB on every ring shape,
+        // e.g. B=64 gamma=8 V=51865 bf16 67.0 -> 59.6 us; 10 KB loses C3 f32)
+        static const int piece_min = getenv("SSV_PIECE_KB") ? atoi(getenv("SSV_PIECE_KB")) * 1024 : 12288;  // experiment knob
+        const bool pieced = NS < NRc && SE * s >= 2 * piece_min;
         static const bool no_gate = getenv("SSV_NO_GATE") != nullptr;  // experiment knob
         if (!no_gate && !(cta_bytes <= 300L * 1024 || (NS >= 4 && cta_bytes <= 600L * 1024) || (P.B >= 48 && cta_bytes <= 520L * 1024) ||
                           (P.B >= 32 && P.V <= 65536 && cta_bytes <= 600L * 1024 && (NS >= 3 || pieced))))
             continue;
-        // A true ring streams pieces of the slices (H per slice, >= 16 KB each):
+        // A true ring streams pieces of the slices (H per slice, >= 12 KB each):
         // a slot is refilled after a piece's fold, not a whole slice's
         // (C3 f32, 32 KB slices in 16 KB pieces: 48.4 -> 44.7 us; 8 KB pieces
         // measured slower than whole 16 KB slices).
         static const int pieces_env = getenv("SSV_PIECES") ? atoi(getenv("SSV_PIECES")) : 0;  // experiment knob
         int H = 1, PE = SE, NSu = NS;
-        const int want_h = pieces_env > 0 ? pieces_env : std::max(1, std::min(4, SE * s / 16384));
+        const int want_h = pieces_env > 0 ? pieces_env : std::max(1, std::min(4, SE * s / piece_min));
         if (NS < NRc && want_h > 1) {
             H = want_h;
             PE = ((SE + H - 1) / H + kGW - 1) / kGW * kGW;
