@@ -1229,21 +1229,25 @@ __global__ void __launch_bounds__(kCtaThreads, kCtaMinBlocks) k_verify(StepParam
 
 // ---------------------------------------------------------------------------
 // K1c/K2c k_verify_cluster<T, ACT>: the cluster path.  One
-// thread-block cluster of cl_size (16, 12, 8 or 4) CTAs per batch row; rank k owns the element
-// slice [k*SE, (k+1)*SE) of every row:
-//   1. exact: one TMA bulk copy per drafted p / q row stages the rank's slice of
-//      the row in a ring of cl_slots shared-memory slots (all rows at once when
-//      they fit), while all threads gather the drafted logits and the
+// thread-block cluster of cl_size (16 down to 4) CTAs per batch row; rank k
+// owns the element slice [k*SE, (k+1)*SE) of every row.  Two plans
+// (plan_cluster_t): resident -- one CTA per SM holding every drafted row
+// slice (small B); ring -- two CTAs per SM streaming the slices (in pieces of
+// >= 12 KB) through cl_slots shared-memory slots.
+//   1. exact: one TMA bulk copy per drafted p / q row slice (or piece) stages
+//      it in a slot, while all threads gather the drafted logits and the
 //      uniforms; one warp per row folds the slice to (max, sum e^(x - max)) as
 //      it lands (FMNMX3; four fp32 sum chains, fp64 in the folds) and restages
-//      the slot it consumed with a later row;
+//      the slot it consumed with a later unit; the slice partials are pushed
+//      into every rank's shared memory;
 //   2. cluster barrier; every CTA folds the cl_size slice partials of every row
-//      through DSMEM in the same fixed order, so all ranks reach the identical
-//      decision (tau in fp64, first rejection) without another exchange;
-//      sigmoid / probabilities: the decision comes from the gathers alone;
-//   3. each rank reduces its slice of the rejected pair / bonus row (L2-hot) to
-//      512-element granule masses and pushes its slice total into every rank's
-//      shared memory (DSMEM stores);
+//      in the same fixed order, so all ranks reach the identical decision (tau
+//      in fp64, first rejection) without another exchange; sigmoid /
+//      probabilities: the decision comes from the gathers alone;
+//   3. each rank reduces its slice of the rejected pair (from shared memory
+//      when resident, else L2-hot) / bonus row (bulk-prefetched into L2) to
+//      512-element granule masses and pushes its slice total into every
+//      rank's shared memory (DSMEM stores);
 //   4. cluster barrier; every rank combines the totals in the same order, and
 //      the rank whose slice holds u * denominator runs the inverse CDF over its
 //      own granules and elements (no DSMEM access after the barrier).
