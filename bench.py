@@ -2,25 +2,36 @@
 """Benchmark of the speculative-sampling verification step (arXiv 2406.11016).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--workload c2] [--variant exact|sigmoid] [--no-extra]
+                    [--workload c4] [--variant exact|sigmoid] [--no-extra] [--no-cpu]
 
-One "step" = one verification call over one batch (B x gamma drafted tokens)
-of synthetic logits made by the reference bench recipe (bench.cpp:46-74,
-global batch row b seeded 1 + b).  Metric (BASELINE.json): verified drafted
-tokens/s = N * B * gamma / max-over-ranks(seconds per step), whole job.
+Workload (default, BASELINE.json config 4): C4 large-vocab verify, global batch
+B=256, gamma=8, V=151936, fp32 logits, exact variant.  With N GPUs (torchrun,
+one rank per GPU) the 256 batch rows are sharded into contiguous slabs, no
+collective on the data path: STRONG scaling (the global batch is fixed).
 
-* value     device-resident inputs, K steps replayed as one CUDA graph, CUDA
-            events on the launching stream; inputs rotate over R copies whose
-            total exceeds 3x L2 so every step reads HBM.
+Inputs: batch row b = the reference's make_bench_inputs(1 + b, gamma, V)
+(bench.cpp:46-74) rounded to the storage type, generated on the host by
+tools/benchgen.c (pinned bit-for-bit to the compiled reference by
+tests/test_benchgen.py).  Both arms consume exactly these bits: the GPU arm
+copies its slab to the device, the reference arm widens a row sample to double.
+
+One "step" = one verification call over the rank's slab.  Metric
+(BASELINE.json): verified drafted tokens/s = B * gamma / max-over-ranks(s/step).
+
+* value     device-resident inputs (> 3x L2 across R rotating copies, so every
+            step reads HBM), K steps replayed as one CUDA graph, CUDA events on
+            the launching stream, barrier + synchronize on both sides.
 * e2e       the same metric through the host C-ABI entry point
-            (ssv_verify_*_host): pinned host logits -> H2D -> kernels -> D2H of
-            every result, synchronized each step.
-* roofline  dominant kernel: algorithmic bytes / its event-timed duration vs
-            MEASURED_PEAKS.json hbm_gbs.
-* cpu_baseline  the reference itself (oracle/_ref, compiled from the reference
-            sources) timed on this host, rank 0 at N=1, bounded sample.
-Multi-GPU: torchrun, one rank per GPU, batch rows sharded with no collective
-on the data path (weak scaling: B rows per GPU).
+            (ssv_verify_*_host via Verifier.prepare_host): pinned host logits
+            -> H2D -> kernel -> results in pinned memory, synchronized per step.
+* roofline  the step is ONE kernel launch: achieved = algorithmic bytes per
+            launch / graph-timed step time, vs MEASURED_PEAKS
+            hbm_gbs; `traffic` = ncu DRAM bytes of the same launch
+            (profiles/ncu_summary.json).
+* cpu_baseline  the compiled reference (oracle/_ref) on a row sample of the
+            same inputs, rank 0 at N=1.
+--impl reference: the compiled reference (pooled materialize_softmax_into +
+verify_fused, or verify_sigmoid_fused) on all host cores, same config dict.
 """
 from __future__ import annotations
 
@@ -37,16 +48,18 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "verified drafted tokens/sec and achieved HBM GB/s (% of roofline), 1/2/4/8 B200"
+# key: (description, GLOBAL batch B, gamma, V, storage); B rows shard over the GPUs
 WORKLOADS = {
-    # key: (description, B per GPU, gamma, V, storage)
     "c1": ("C1 exact verify B=1 gamma=5 V=32000 fp32 (reference CPU workload)", 1, 5, 32000, "f32"),
     "c2": ("C2 Whisper-shape ASR verify B=8 gamma=5 V=51865 fp32", 8, 5, 51865, "f32"),
     "c3": ("C3 Llama-2-shape verify B=64 gamma=8 V=32000 fp32", 64, 8, 32000, "f32"),
     "c3bf16": ("C3 Llama-2-shape verify B=64 gamma=8 V=32000 bf16", 64, 8, 32000, "bf16"),
-    "c4": ("C4 large-vocab verify B=256 gamma=8 V=151936 fp32 (per GPU)", 256, 8, 151936, "f32"),
-    "c4shard": ("C4 large-vocab verify B=32/GPU (256 over 8 GPUs) gamma=8 V=151936 fp32", 32, 8, 151936, "f32"),
-    "c4bf16": ("C4 large-vocab verify B=256 gamma=8 V=151936 bf16 (per GPU)", 256, 8, 151936, "bf16"),
+    "c4": ("C4 large-vocab verify B=256 gamma=8 V=151936 fp32, batch-sharded over the GPUs", 256, 8, 151936, "f32"),
+    "c4bf16": ("C4 large-vocab verify B=256 gamma=8 V=151936 bf16, batch-sharded over the GPUs", 256, 8, 151936,
+               "bf16"),
+    "c4shard": ("C4 one GPU's share on 8xB200: B=32 gamma=8 V=151936 fp32", 32, 8, 151936, "f32"),
 }
+SEED = 1
 BYTES = {"f32": 4, "bf16": 2, "f64": 8}
 
 
@@ -127,29 +140,75 @@ class ClockSampler:
                 "reasons": sorted(self.reasons), "samples": len(self.samples)}
 
 
-# ----------------------------------------------------------------------------- device arm
+# ----------------------------------------------------------------------------- workload
+def config_dict(key, variant, world):
+    """The config both arms print (identical keys and values)."""
+    desc, B, gamma, V, storage = WORKLOADS[key]
+    return {"workload": desc, "variant": variant, "global_batch": B, "gamma": gamma, "V": V, "storage": storage,
+            "seed": SEED, "parallelism": f"batch rows sharded over {world} GPU(s) (strong scaling), no collective"}
+
+
+def algorithmic_bytes(variant, B, gamma, V, s, accepted_len):
+    """exact s*V*(2*gamma*B + A) + small terms; sigmoid
+    s*V*(A + 2R) + gathered logits + small terms; A = rows accepting all gamma."""
+    import numpy as np
+
+    acc = np.asarray(accepted_len)
+    A = int((acc == gamma).sum())
+    R = B - A
+    small = 4 * B * gamma + 8 * B * (gamma + 1) + (17 + 8 * gamma) * B
+    if variant == "exact":
+        return s * V * (2 * gamma * B + A) + small, A
+    return s * V * (A + 2 * R) + 2 * s * B * gamma + small, A
+
+
 class Workload:
-    def __init__(self, v, key, rank, variant, rotate=True, world=1):
+    """This rank's slab of the global batch: pinned host copy (tools/benchgen)
+    + R device copies rotating so that every step reads HBM."""
+
+    def __init__(self, v, key, rank, world, variant, host_gen=True, rotate=True):
+        import numpy as np
         import torch
 
-        from paper_2406_11016_b200.shard import shard_range, slab_seed
+        from paper_2406_11016_b200.shard import shard_range
 
-        desc, B, gamma, V, storage = WORKLOADS[key]
-        self.key, self.desc, self.B, self.gamma, self.V, self.storage = key, desc, B, gamma, V, storage
-        self.variant = variant
+        desc, Bg, gamma, V, storage = WORKLOADS[key]
+        self.key, self.desc, self.gamma, self.V, self.storage, self.variant = key, desc, gamma, V, storage, variant
+        # Fewer batch rows than GPUs (C1, C2 at N = 8): independent replicas
+        self.replicas = Bg < world
+        self.lo, self.hi = (0, Bg) if self.replicas else shard_range(Bg, world, rank)
+        self.B = self.hi - self.lo
         self.s = BYTES[storage]
         tdt = {"f32": torch.float32, "bf16": torch.bfloat16}[storage]
-        # weak scaling: B rows per GPU, global row b seeded 1 + b (bench.cpp:46-74)
-        lo, hi = shard_range(world * B, world, rank)
-        zp, zq, ids, u = v.make_bench_inputs(slab_seed(1, lo), hi - lo, gamma, V, tdt)
+        B = self.B
+        self.host = None
+        if host_gen:
+            from tools import benchgen
+
+            npdt = np.float32 if storage == "f32" else np.uint16
+            h = (v.host_empty((B, gamma + 1, V), npdt), v.host_empty((B, gamma, V), npdt),
+                 v.host_empty((B, gamma), np.int32), v.host_empty((B, gamma + 1), np.float64))
+            t0 = time.perf_counter()
+            benchgen.make_bench_batch(SEED + self.lo, B, gamma, V, storage, out=h)
+            log(f"[bench] {key}: host inputs rows {self.lo}..{self.hi} in {time.perf_counter() - t0:.1f} s")
+            self.host = h
+            dev = torch.device("cuda", torch.cuda.current_device())
+            zp = torch.from_numpy(h[0]).to(dev, non_blocking=True)
+            zq = torch.from_numpy(h[1]).to(dev, non_blocking=True)
+            if storage == "bf16":
+                zp, zq = zp.view(torch.bfloat16), zq.view(torch.bfloat16)
+            ids = torch.from_numpy(h[2]).to(dev)
+            u = torch.from_numpy(h[3]).to(dev)
+            self.inputs = "host generator tools/benchgen.c (= reference make_bench_inputs, rounded)"
+        else:
+            zp, zq, ids, u = v.make_bench_inputs(SEED + self.lo, B, gamma, V, tdt)
+            self.inputs = "device generator ssv_make_bench_inputs"
         torch.cuda.synchronize()
         self.set_bytes = (zp.numel() + zq.numel()) * self.s
-        l2 = torch.cuda.get_device_properties(torch.cuda.current_device()).L2_cache_size
-        self.l2 = l2
-        R = max(2, math.ceil(3 * l2 / self.set_bytes)) if rotate else 1
-        R = min(R, max(1, int(40e9 // self.set_bytes)))
-        self.R = R
-        self.sets = [(zp, zq, ids, u)] + [(zp.clone(), zq.clone(), ids.clone(), u.clone()) for _ in range(R - 1)]
+        self.l2 = torch.cuda.get_device_properties(torch.cuda.current_device()).L2_cache_size
+        R = max(2, math.ceil(3 * self.l2 / self.set_bytes)) if rotate else 1
+        self.R = min(R, max(1, int(40e9 // self.set_bytes)))
+        self.sets = [(zp, zq, ids, u)] + [(zp.clone(), zq.clone(), ids.clone(), u.clone()) for _ in range(self.R - 1)]
         self.outs = None
 
     def call(self, v, k, out=None):
@@ -157,22 +216,6 @@ class Workload:
         if self.variant == "exact":
             return v.verify_exact(zp, zq, ids, u, out=out)
         return v.verify_sigmoid(zp, zq, ids, u, -1e3, 1e3, out=out)
-
-    def algorithmic_bytes(self, res):
-        """SURVEY.md 8(d): exact s*V*(2*gamma*B + A) + small terms;
-        sigmoid s*V*(A + 2R) + gathers; A = rows that accepted all gamma."""
-        import numpy as np
-
-        acc = np.asarray(res.accepted_len.cpu())
-        A = int((acc == self.gamma).sum())
-        Rr = self.B - A
-        B, g, V, s = self.B, self.gamma, self.V, self.s
-        small = 4 * B * g + 8 * B * (g + 1) + (17 + 8 * g) * B
-        if self.variant == "exact":
-            step = s * V * (2 * g * B + A) + small
-        else:
-            step = s * V * (A + 2 * Rr) + 2 * s * B * g + small
-        return step, step, A
 
 
 def acceptance(v, wl):
@@ -203,16 +246,23 @@ def capture(v, wl, steps, stream):
     return g
 
 
+def _barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+
+
 def measure_device(v, wl, K, W, world, sampler=None):
-    """Returns dict(ms_per_step, kernel_ms, launches, result)."""
+    """K steps replayed as one CUDA graph; returns ms per step, launches per
+    step and the first set's result."""
     import torch
 
     stream = torch.cuda.Stream()
     v.set_stream(stream)
-    # outputs per rotating set; first call also sizes the context scratch
     wl.outs = [None] * wl.R
     with torch.cuda.stream(stream):
-        for k in range(wl.R):
+        for k in range(wl.R):  # sizes the context scratch; results per rotating set
             wl.outs[k] = wl.call(v, k)
     stream.synchronize()
     launches_per_step = v.last_launch_count
@@ -221,42 +271,22 @@ def measure_device(v, wl, K, W, world, sampler=None):
         raise RuntimeError(f"device status {st} on the synthetic inputs")
     g_warm = capture(v, wl, max(W, 1), stream)
     g_time = capture(v, wl, K, stream)
-    # kernel timing: an instrumented replica of the timed graph
-    v.profile_enable(K * launches_per_step + 8)
-    g_prof = capture(v, wl, K, stream)
-    v.profile_disable()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-
-    def barrier():
-        if world > 1:
-            import torch.distributed as dist
-
-            dist.barrier()
-
     with torch.cuda.stream(stream):
         g_warm.replay()
         stream.synchronize()
-        barrier()
+        _barrier(world)
         torch.cuda.synchronize()
-        ctx = sampler if sampler is not None else _Null()
-        with ctx:
+        with (sampler if sampler is not None else _Null()):
             e0.record(stream)
             g_time.replay()
             e1.record(stream)
             stream.synchronize()
-        barrier()
+        _barrier(world)
         torch.cuda.synchronize()
-        ms = e0.elapsed_time(e1)
-        g_prof.replay()
-        stream.synchronize()
-    kern = {}
-    for kid, name in ((0, "k_verify"), (2, "k_materialize")):
-        tot, n = v.profile_read(kid)
-        if n:
-            kern[name] = tot / n
+    ms = e0.elapsed_time(e1)
     v.set_stream(None)  # back to following torch's current stream
-    return {"ms_per_step": ms / K, "kernel_ms": kern, "launches_per_step": launches_per_step,
-            "result": wl.outs[0]}
+    return {"ms_per_step": ms / K, "launches_per_step": launches_per_step, "result": wl.outs[0]}
 
 
 class _Null:
@@ -267,149 +297,140 @@ class _Null:
         pass
 
 
-def measure_e2e(v, wl, K, W):
-    """Host entry point: pinned host inputs -> H2D -> step -> D2H, sync per step."""
+def measure_e2e(v, wl, K, W, world):
+    """Host entry point: pinned host inputs -> H2D -> step -> results in pinned
+    memory, synchronized per step (the serving-loop form, Verifier.prepare_host)."""
     import numpy as np
-    import torch
 
-    zp, zq, ids, u = wl.sets[0]
-    hz = {}
-    for name, t in (("zp", zp), ("zq", zq)):
-        a = v.host_empty(tuple(t.shape), np.uint16 if wl.storage == "bf16" else np.float32)
-        a[...] = (t.view(torch.int16).cpu().numpy().view(np.uint16) if wl.storage == "bf16" else t.cpu().numpy())
-        hz[name] = a
-    hids = v.host_empty(tuple(ids.shape), np.int32)
-    hids[...] = ids.cpu().numpy()
-    hu = v.host_empty(tuple(u.shape), np.float64)
-    hu[...] = u.cpu().numpy()
-    B, g = wl.B, wl.gamma
     from paper_2406_11016_b200.ssv import VerifyResult
 
+    hzp, hzq, hids, hu = wl.host
+    B, g = wl.B, wl.gamma
     out = VerifyResult(v.host_empty((B,), np.int32), v.host_empty((B,), np.int32), v.host_empty((B,), np.uint8),
                        v.host_empty((B, g), np.float64), v.host_empty((B,), np.float64),
                        status=v.host_empty((1,), np.uint32))
     dt = "bfloat16" if wl.storage == "bf16" else None
-    # Verifier.prepare_host: the serving-loop form of verify_*_host (argument
-    # structs built once over the pinned buffers; each call is one C-ABI call)
-    step = v.prepare_host(wl.variant, hz["zp"], hz["zq"], hids, hu, out, dtype=dt)
+    step = v.prepare_host(wl.variant, hzp, hzq, hids, hu, out, dtype=dt)
     for _ in range(W):
         step()
+    _barrier(world)
     t0 = time.perf_counter()
     for _ in range(K):
         step()
     t = (time.perf_counter() - t0) / K
-    h2d = hz["zp"].nbytes + hz["zq"].nbytes + hids.nbytes + hu.nbytes
+    if int(out.status[0]):
+        raise RuntimeError(f"e2e: device status {int(out.status[0])}")
+    h2d = hzp.nbytes + hzq.nbytes + hids.nbytes + hu.nbytes
     d2h = B * 4 + B * 4 + B + B * g * 8 + B * 8 + 4
-    return t, h2d, d2h, v.last_launch_count
+    return t, h2d, d2h
 
 
-# ----------------------------------------------------------------------------- CPU arm
-def cpu_inputs(wl):
-    zp, zq, ids, u = wl.sets[0]
-    return (zp.double().cpu().numpy(), zq.double().cpu().numpy(), ids.cpu().numpy(), u.cpu().numpy())
-
-
-def cpu_time(zp, zq, ids, u, gamma, variant, budget_s, workers):
-    """Time the reference's CPU path (oracle/_ref if built, else the C port) on
-    a bounded row sample.  Returns dict for the JSON line."""
+# ----------------------------------------------------------------------------- CPU (reference) arm
+def time_reference(zp, zq, ids, u, variant, budget_s, workers, warmup=1, trials=None):
+    """The compiled reference (oracle/_ref) on a row sample of the given (double)
+    inputs: pooled materialize_softmax_into + verify_fused (exact) or
+    verify_sigmoid_fused (sigmoid) on WorkerPool(workers), tile 1024.  Rows
+    are independent (verify_reference.cpp:87-109), so the sample's per-row
+    rate is the workload's.  Returns (tokens/s, median s/step, rows, trials)."""
     import numpy as np
 
-    from oracle.oracle import Oracle, Ref, ref_available
+    from oracle.oracle import Ref
 
+    ref = Ref()
+    backend = 1 if variant == "exact" else 2
+    gamma = zq.shape[1]
     B = zp.shape[0]
-    if ref_available():
-        ref = Ref()
-        backend = 1 if variant == "exact" else 2
-        # one probe step on one row to size the sample
-        ns, _ = ref.time_backend(backend, zp[:1], zq[:1], ids[:1], u[:1], workers=workers, warmup=0, trials=1)
-        per_row = ns[0] * 1e-9
+    ns, _ = ref.time_backend(backend, zp[:1], zq[:1], ids[:1], u[:1], workers=workers, warmup=0, trials=1)
+    per_row = ns[0] * 1e-9
+    if trials is None:
         rows = int(max(1, min(B, budget_s / 4 / max(per_row, 1e-9))))
         trials = int(max(3, min(30, budget_s / max(per_row * rows, 1e-9))))
-        ns, _ = ref.time_backend(backend, zp[:rows], zq[:rows], ids[:rows], u[:rows], workers=workers,
-                                 warmup=1, trials=trials)
-        t = float(np.median(ns)) * 1e-9
-        name = ("pooled materialize_softmax_into + verify_fused" if variant == "exact"
-                else "verify_sigmoid_fused")
-        return {"value": rows * gamma / t, "unit": "tokens/s", "cores": workers, "kind": "reference",
-                "sample": f"{rows} of {B} batch rows, median of {trials} steps, {name} "
-                          f"(WorkerPool({workers}), tile 1024), oracle/_ref compiled from the reference sources"}
-    o = Oracle()
-    rows = 1
-    t0 = time.perf_counter()
-    n = 0
-    while time.perf_counter() - t0 < budget_s / 2 or n < 3:
-        if variant == "exact":
-            o.verify_exact(zp[:rows], zq[:rows], ids[:rows], u[:rows])
-        else:
-            o.verify_sigmoid(zp[:rows], zq[:rows], ids[:rows], u[:rows], -1e3, 1e3)
-        n += 1
-    t = (time.perf_counter() - t0) / n
-    return {"value": rows * gamma / t, "unit": "tokens/s", "cores": 1, "kind": "port",
-            "sample": f"1 of {B} batch rows x {n} steps, oracle/ssv_oracle.c (sequential)"}
+    else:
+        rows = int(max(1, min(B, budget_s / (trials + warmup) / max(per_row, 1e-9))))
+    ns, _ = ref.time_backend(backend, zp[:rows], zq[:rows], ids[:rows], u[:rows], workers=workers, warmup=warmup,
+                             trials=trials)
+    t = float(np.median(ns)) * 1e-9
+    return rows * gamma / t, t, rows, trials
+
+
+def reference_sample(key, rows_max):
+    """The first rows of the global batch, the same bits the GPU arm uses, widened to double."""
+    from tools import benchgen
+
+    desc, B, gamma, V, storage = WORKLOADS[key]
+    n = min(B, rows_max)
+    zp, zq, ids, u = benchgen.make_bench_batch(SEED, n, gamma, V, storage)
+    return benchgen.widen(zp, storage), benchgen.widen(zq, storage), ids, u
+
+
+def ref_name(variant, workers):
+    return ((f"pooled materialize_softmax_into + verify_fused" if variant == "exact" else "verify_sigmoid_fused") +
+            f" on WorkerPool({workers}), tile 1024, oracle/_ref (the reference compiled from its sources)")
 
 
 def run_reference_arm(args):
-    """bench.py --impl reference: the reference's own CPU path, rank 0 only."""
-    rank = int(os.environ.get("RANK", "0"))
-    if rank != 0:
+    """bench.py --impl reference: the reference's own CPU path on this host,
+    rank 0 only (other ranks exit without work)."""
+    if int(os.environ.get("RANK", "0")) != 0:
         return
-    import numpy as np
-
-    from oracle.oracle import Oracle, Ref, ref_available
+    from oracle.oracle import ref_available
 
     desc, B, gamma, V, storage = WORKLOADS[args.workload]
-    N = args.gpus
-    o = Oracle()
-    zp, zq, ids, u = o.make_bench_batch(1, B, gamma, V)
-    zp = o.round_f32(zp) if storage == "f32" else o.round_bf16(zp)
-    zq = o.round_f32(zq) if storage == "f32" else o.round_bf16(zq)
+    cfg = config_dict(args.workload, args.variant, args.gpus)
+    if not ref_available():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built (reference sources absent)"}))
+        return
     workers = os.cpu_count() or 1
     budget = 150.0  # seconds for the whole --steps run
-    if ref_available():
-        ref = Ref()
-        backend = 1 if args.variant == "exact" else 2
-        ns, _ = ref.time_backend(backend, zp[:1], zq[:1], ids[:1], u[:1], workers=workers, warmup=0, trials=1)
-        per_row = ns[0] * 1e-9
-        rows = int(max(1, min(B, budget / (args.steps + args.warmup) / max(per_row, 1e-9))))
-        ns, _ = ref.time_backend(backend, zp[:rows], zq[:rows], ids[:rows], u[:rows], workers=workers,
-                                 warmup=args.warmup, trials=args.steps)
-        kind = "reference"
-        sample = (f"{rows} of {B} batch rows per step, reference "
-                  f"{'pooled softmax + verify_fused' if args.variant == 'exact' else 'verify_sigmoid_fused'} "
-                  f"on WorkerPool({workers})")
-        t = float(np.median(ns)) * 1e-9
-    else:
-        rows, kind, workers = 1, "port", 1
-        times = []
-        for i in range(args.warmup + args.steps):
-            t0 = time.perf_counter()
-            o.verify_exact(zp[:1], zq[:1], ids[:1], u[:1])
-            if i >= args.warmup:
-                times.append(time.perf_counter() - t0)
-        t = statistics.median(times)
-        sample = "1 batch row per step, oracle port (sequential)"
-    value = rows * gamma / t
-    line = {"metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": N, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak",
+    zp, zq, ids, u = reference_sample(args.workload, 64)
+    value, t, rows, trials = time_reference(zp, zq, ids, u, args.variant, budget, workers, warmup=args.warmup,
+                                            trials=args.steps)
+    sample = (f"{rows} of the {B} batch rows per step (rows independent: per-row rate = workload rate), "
+              f"median of {trials} steps after {args.warmup} warm-up, {ref_name(args.variant, workers)}; "
+              f"inputs: tools/benchgen.c rows = make_bench_inputs(1 + b) rounded to {storage}, widened to double")
+    line = {"metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (make_bench_inputs, bench.cpp:46-74)",
-            "config": {"workload": desc, "variant": args.variant, "B": B, "gamma": gamma, "V": V},
-            "impl": "reference",
-            "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": workers, "kind": kind, "sample": sample},
+            "config": cfg, "impl": "reference",
+            "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": workers, "kind": "reference",
+                             "sample": sample},
             "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
 # ----------------------------------------------------------------------------- main
+EXTRAS = (("c4", "sigmoid"), ("c4bf16", "exact"), ("c4shard", "exact"), ("c3", "exact"), ("c3bf16", "exact"),
+          ("c3", "sigmoid"), ("c2", "exact"), ("c2", "sigmoid"), ("c1", "exact"), ("c1", "sigmoid"))
+
+
+def extra_line(v, key, variant, peak):
+    import torch
+
+    w2 = Workload(v, key, 0, 1, variant, host_gen=False)
+    K = 50 if w2.B * w2.V > 1e7 else 200
+    m2 = measure_device(v, w2, K, 5, 1)
+    r = m2["result"].numpy()
+    kb, A2 = algorithmic_bytes(variant, w2.B, w2.gamma, w2.V, w2.s, r.accepted_len)
+    ms = m2["ms_per_step"]
+    d = {"tokens_per_s": w2.B * w2.gamma / (ms * 1e-3), "ms_per_step": ms, "gbs": kb / (ms * 1e-3) / 1e9,
+         "frac": kb / (ms * 1e-3) / 1e9 / peak, "algorithmic_bytes": kb, "accepted_all_rows": A2, "B": w2.B,
+         "launches_per_step": m2["launches_per_step"], "inputs": w2.inputs}
+    del w2
+    torch.cuda.empty_cache()
+    return d
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=2000)
-    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
+    ap.add_argument("--workload", default="c4", choices=sorted(WORKLOADS))
     ap.add_argument("--variant", default="exact", choices=["exact", "sigmoid"])
     ap.add_argument("--no-extra", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")
@@ -427,28 +448,34 @@ def main():
 
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_2406_11016_b200 import Verifier
-
-    v = Verifier(local)
-    peak, peak_src = load_peaks()
-    wl = Workload(v, args.workload, rank, args.variant, world=world)
-    sampler = ClockSampler(local)
-    m = measure_device(v, wl, args.steps, args.warmup, world, sampler)
-    step_bytes, k_bytes, A = wl.algorithmic_bytes(m["result"])
-
-    e2e_t, h2d, d2h, e2e_launches = measure_e2e(v, wl, max(3, min(args.steps, 50)), 3)
-
     from paper_2406_11016_b200.shard import allmax as _allmax
 
     def allmax(x):
         return _allmax(x, device="cuda")
 
+    v = Verifier(local)
+    peak, peak_src = load_peaks()
+    desc, Bg, gamma, V, storage = WORKLOADS[args.workload]
+    wl = Workload(v, args.workload, rank, world, args.variant)
+    sampler = ClockSampler(local)
+    m = measure_device(v, wl, args.steps, args.warmup, world, sampler)
+    res = m["result"].numpy()
+    k_bytes, A = algorithmic_bytes(args.variant, wl.B, gamma, V, wl.s, res.accepted_len)
     ms = allmax(m["ms_per_step"])
-    e2e_t = allmax(e2e_t)
-    tokens = world * wl.B * wl.gamma
-    dom = "k_verify"
-    kms = m["kernel_ms"].get(dom)
-    achieved = k_bytes / (kms * 1e-3) / 1e9 if kms else None
-    traffic = load_traffic(f"{args.workload}-{args.variant}")
+    k_ms_local = m["ms_per_step"]
+    tokens = (world if wl.replicas else 1) * Bg * gamma
+    e2e = None
+    if not args.no_e2e:
+        ke = max(3, min(args.steps, 20))
+        e2e_t, h2d, d2h = measure_e2e(v, wl, ke, 2, world)
+        e2e_t = allmax(e2e_t)
+        e2e = {"value": tokens / e2e_t, "unit": "tokens/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+               "ms_per_step": e2e_t * 1e3, "steps": ke,
+               "path": f"ssv_verify_{args.variant}_host via Verifier.prepare_host (C-ABI host entry on pinned host "
+                       "buffers: H2D of the step's inputs + verify; the kernel writes the small results into pinned "
+                       "memory; synchronized per step), per-rank bytes"}
+    achieved = k_bytes / (k_ms_local * 1e-3) / 1e9
+    traffic = load_traffic(f"{args.workload}-{args.variant}") if world == 1 else None
     line = {
         "metric": METRIC,
         "value": tokens / (ms * 1e-3),
@@ -458,65 +485,58 @@ def main():
         "warmup": args.warmup,
         "ms_per_step": ms,
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": "weak" if wl.replicas else "strong",
         "vs_baseline": None,
-        "dtype": wl.storage,
+        "dtype": storage,
         "data": "synthetic logits by the reference bench recipe (bench.cpp:46-74), global batch row b seeded 1+b",
-        "config": {
-            "workload": wl.desc, "variant": args.variant, "B_per_gpu": wl.B, "global_batch": world * wl.B,
-            "gamma": wl.gamma, "V": wl.V, "parallelism": f"batch rows sharded over {world} GPU(s), no collective",
+        "config": config_dict(args.workload, args.variant, world),
+        "details": {
+            "rows_this_rank": [wl.lo, wl.hi], "inputs": wl.inputs,
             "l2": f"inputs rotate over {wl.R} copies ({wl.R * wl.set_bytes / 1e6:.0f} MB > 3x L2 "
-                  f"{wl.l2 / 1e6:.0f} MB), every step reads HBM",
+                  f"{wl.l2 / 1e6:.0f} MB): every step reads HBM",
             "timing": "K steps replayed as one CUDA graph, CUDA events on the launching stream, max over ranks",
         },
         "gpu_launches": args.steps * m["launches_per_step"],
-        "hbm_gbs_step": step_bytes / (ms * 1e-3) / 1e9,
         "accepted_all_rows": A,
         "acceptance_rate": acceptance(v, wl),
-        "e2e": {"value": tokens / e2e_t, "unit": "tokens/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                "ms_per_step": e2e_t * 1e3,
-                "path": "ssv_verify_%s_host via Verifier.prepare_host (C-ABI host entry, pinned host buffers, H2D + verify, results written to pinned memory by the kernel, sync per step)" % args.variant},
         "roofline": {
-            "bound": "hbm", "kernel": dom,
-            "achieved": achieved, "peak": peak, "unit": "GB/s",
-            "frac": (achieved / peak) if achieved else None,
+            "bound": "hbm", "kernel": "ssv verify kernel (one launch per step)",
+            "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
             "traffic": traffic.get("dram_bytes_per_launch") if traffic else None,
-            "algorithmic_bytes_per_launch": k_bytes,
-            "kernel_ms": kms, "peak_source": peak_src,
-            "kernels_ms": m["kernel_ms"],
+            "algorithmic_bytes_per_launch": k_bytes, "kernel_ms": k_ms_local,
+            "kernel_ms_source": "graph-timed step (the step is one launch; PDL overlaps consecutive launches)",
+            "ncu_kernel_ms": (traffic.get("duration_ns") / 1e6 if traffic and traffic.get("duration_ns") else None),
+            "peak_source": peak_src,
         },
         "clocks": sampler.summary(),
     }
+    if e2e:
+        line["e2e"] = e2e
     if rank == 0 and world == 1 and not args.no_cpu:
         try:
-            zp, zq, ids, u = cpu_inputs(wl)
-            line["cpu_baseline"] = cpu_time(zp, zq, ids, u, wl.gamma, args.variant, 12.0, os.cpu_count() or 1)
+            from oracle.oracle import ref_available
+
+            if ref_available():
+                zp = wl.host[0][:16]
+                zq = wl.host[1][:16]
+                from tools import benchgen
+
+                val, t, rows, trials = time_reference(benchgen.widen(zp, storage), benchgen.widen(zq, storage),
+                                                      wl.host[2][:16], wl.host[3][:16], args.variant, 12.0,
+                                                      os.cpu_count() or 1)
+                line["cpu_baseline"] = {
+                    "value": val, "unit": "tokens/s", "cores": os.cpu_count() or 1, "kind": "reference",
+                    "sample": f"{rows} of {Bg} batch rows (the same input bits), median of {trials} steps, "
+                              + ref_name(args.variant, os.cpu_count() or 1)}
         except Exception as e:  # the baseline is reported, never required
             line["cpu_baseline"] = {"value": None, "error": str(e)}
     if rank == 0 and world == 1 and not args.no_extra:
         extra = {}
-        for key, variant in (("c2", "sigmoid" if args.variant == "exact" else "exact"), ("c1", "exact"),
-                             ("c1", "sigmoid"), ("c3", "exact"), ("c3bf16", "exact"), ("c3", "sigmoid"),
-                             ("c3bf16", "sigmoid"), ("c4", "exact"), ("c4", "sigmoid"), ("c4bf16", "exact"),
-                             ("c4shard", "exact")):
+        for key, variant in EXTRAS:
             if key == args.workload and variant == args.variant:
                 continue
             try:
-                w2 = Workload(v, key, 0, variant)
-                m2 = measure_device(v, w2, 200, 5, 1)
-                sb, kb, A2 = w2.algorithmic_bytes(m2["result"])
-                d = "k_verify"
-                km = m2["kernel_ms"].get(d)
-                extra[f"{key}-{variant}"] = {
-                    "tokens_per_s": w2.B * w2.gamma / (m2["ms_per_step"] * 1e-3),
-                    "ms_per_step": m2["ms_per_step"], "step_gbs": sb / (m2["ms_per_step"] * 1e-3) / 1e9,
-                    "kernel": d, "kernel_ms": km,
-                    "kernel_gbs": kb / (km * 1e-3) / 1e9 if km else None,
-                    "kernel_frac": kb / (km * 1e-3) / 1e9 / peak if km else None,
-                    "kernels_ms": m2["kernel_ms"], "accepted_all_rows": A2, "B": w2.B,
-                }
-                del w2
-                torch.cuda.empty_cache()
+                extra[f"{key}-{variant}"] = extra_line(v, key, variant, peak)
             except Exception as e:
                 extra[f"{key}-{variant}"] = {"error": str(e)}
         line["extra"] = extra

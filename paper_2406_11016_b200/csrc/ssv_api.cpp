@@ -40,7 +40,15 @@ struct ssv_ctx {
     unsigned long long* trace = nullptr;  // diagnostics (ssv_debug_trace)
     int trace_cap = 0;
     uint32_t* status_mirror = nullptr;    // set by run_host for the duration of its launch
-    Launch launcher() { return Launch{stream, &launches, profiling ? &prof : nullptr}; }
+    // Stream hand-over: the scratch and counters are shared by every launch of
+    // the context, so a launch on a new stream must follow the last launch on
+    // the previous one (ssv_set_stream records / waits on this event).
+    cudaEvent_t handover = nullptr;
+    bool dirty = false;  // a launch was issued on `stream` since the last hand-over
+    Launch launcher() {
+        dirty = true;
+        return Launch{stream, &launches, profiling ? &prof : nullptr};
+    }
 };
 
 namespace {
@@ -123,7 +131,8 @@ int ensure_scratch(ssv_ctx* ctx, size_t bytes, size_t counters_n) {
         ctx->counters = nullptr;
         const size_t nn = std::max(counters_n, ctx->counters_n * 2);
         CK(cudaMalloc(&ctx->counters, (2 + 3 * nn) * sizeof(unsigned)));
-        CK(cudaMemset(ctx->counters, 0, (2 + 3 * nn) * sizeof(unsigned)));
+        // on the context's stream: the kernels that read the counters follow it
+        CK(cudaMemsetAsync(ctx->counters, 0, (2 + 3 * nn) * sizeof(unsigned), ctx->stream));
         ctx->counters_n = nn;
     }
     return SSV_OK;
@@ -355,6 +364,7 @@ int ssv_create(int device, ssv_ctx** out) {
         cudaStreamCreateWithFlags(&ctx->own, cudaStreamNonBlocking) != cudaSuccess ||
         cudaMalloc(&ctx->status_dev, sizeof(uint32_t)) != cudaSuccess ||
         cudaMemset(ctx->status_dev, 0, sizeof(uint32_t)) != cudaSuccess ||
+        cudaEventCreateWithFlags(&ctx->handover, cudaEventDisableTiming) != cudaSuccess ||
         cudaMallocHost(&ctx->status_host, sizeof(uint32_t)) != cudaSuccess) {
         ssv_destroy(ctx);
         return SSV_ECUDA;
@@ -383,13 +393,30 @@ void ssv_destroy(ssv_ctx* ctx) {
     if (ctx->stage) cudaFree(ctx->stage);
     if (ctx->hstage) cudaFreeHost(ctx->hstage);
     if (ctx->status_host) cudaFreeHost(ctx->status_host);
+    if (ctx->handover) cudaEventDestroy(ctx->handover);
     if (ctx->own) cudaStreamDestroy(ctx->own);
     delete ctx;
 }
 
 int ssv_set_stream(ssv_ctx* ctx, void* stream) {
     if (!ctx) return SSV_EINVAL;
-    ctx->stream = static_cast<cudaStream_t>(stream);  // NULL: the legacy default stream, as in CUDA
+    cudaStream_t next = static_cast<cudaStream_t>(stream);  // NULL: the legacy default stream, as in CUDA
+    if (next != ctx->stream && ctx->dirty) {
+        // Order the new stream after the context's last launch on the old one
+        // (they share scratch and counters).  Under graph capture on either
+        // side there is nothing to order here: captured work runs when the
+        // graph is launched, on the stream it is launched on.
+        CK(cudaSetDevice(ctx->device));
+        cudaStreamCaptureStatus a = cudaStreamCaptureStatusNone, b = cudaStreamCaptureStatusNone;
+        CK(cudaStreamIsCapturing(ctx->stream, &a));
+        CK(cudaStreamIsCapturing(next, &b));
+        if (a == cudaStreamCaptureStatusNone && b == cudaStreamCaptureStatusNone) {
+            CK(cudaEventRecord(ctx->handover, ctx->stream));
+            CK(cudaStreamWaitEvent(next, ctx->handover, 0));
+        }
+        ctx->dirty = false;
+    }
+    ctx->stream = next;
     return SSV_OK;
 }
 
@@ -471,7 +498,8 @@ int ssv_debug_trace(ssv_ctx* ctx, int capacity, unsigned long long* host_out, in
     ctx->trace_cap = 0;
     if (capacity > 0) {
         CK(cudaMalloc(&ctx->trace, (size_t)capacity * 8));
-        CK(cudaMemset(ctx->trace, 0, (size_t)capacity * 8));
+        CK(cudaMemsetAsync(ctx->trace, 0, (size_t)capacity * 8, ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
         ctx->trace_cap = capacity;
     }
     (void)grid_out;
@@ -558,6 +586,7 @@ int ssv_make_bench_inputs(ssv_ctx* ctx, uint64_t seed, int32_t B, int32_t gamma,
     if (rc) return rc;
     double* draft_u = reinterpret_cast<double*>(static_cast<char*>(ctx->scratch) + L.extra);
     int launches = 0;
+    ctx->dirty = true;
     const Launch lau{ctx->stream, &launches, ctx->profiling ? &ctx->prof : nullptr};
     launch_gen_logits(dtype, seed, B, gamma, V, z_p, z_q, lau);
     launch_gen_uniforms(seed, B, gamma, V, draft_u, uniforms, lau);

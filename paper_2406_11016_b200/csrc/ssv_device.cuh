@@ -164,6 +164,15 @@ __device__ __forceinline__ float fmin3f(float a, float b, float c) {
     asm("min.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
     return r;
 }
+// NaN-propagating minimum: the running minimum of a statistics pass doubles as
+// its non-finite detector (require_finite, dist.cpp:27-36) -- a NaN anywhere in
+// the inputs makes it NaN even where max / sum drop NaN operands.
+__device__ __forceinline__ float fmin3f_nan(float a, float b, float c) {
+    float r;
+    asm("min.NaN.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+    return r;
+}
+__device__ __forceinline__ double fmin_nan(double a, double b) { return (a != a || b != b) ? a + b : fmin(a, b); }
 
 // ---- warp / block reductions (fixed topology) ------------------------------
 template <typename V>

@@ -217,8 +217,8 @@ struct AStat<float> {
                     d = __uint_as_float(v.w);
         m = fmax3f(m, a, b);
         m = fmax3f(m, c, d);
-        n = fmin3f(n, a, b);
-        n = fmin3f(n, c, d);
+        n = fmin3f_nan(n, a, b);
+        n = fmin3f_nan(n, c, d);
     }
     static __device__ __forceinline__ void expsum(const uint4& v, float2 negM, float2& s) {
         const float2 l2e = make_float2(1.4426950408889634f, 1.4426950408889634f);
@@ -238,16 +238,16 @@ struct AStat<__nv_bfloat16> {
         asm("max.bf16x2 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
         return r;
     }
-    static __device__ __forceinline__ uint32_t min2(uint32_t a, uint32_t b) {
+    static __device__ __forceinline__ uint32_t min2(uint32_t a, uint32_t b) {  // NaN-propagating (detector)
         uint32_t r;
-        asm("min.bf16x2 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
+        asm("min.NaN.bf16x2 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
         return r;
     }
     static __device__ __forceinline__ void minmax(const uint4& v, float& m, float& n) {
         const uint32_t mx = max2(max2(v.x, v.y), max2(v.z, v.w));
         const uint32_t mi = min2(min2(v.x, v.y), min2(v.z, v.w));
         m = fmax3f(m, __uint_as_float(mx << 16), __uint_as_float(mx & 0xffff0000u));
-        n = fmin3f(n, __uint_as_float(mi << 16), __uint_as_float(mi & 0xffff0000u));
+        n = fmin3f_nan(n, __uint_as_float(mi << 16), __uint_as_float(mi & 0xffff0000u));
     }
     static __device__ __forceinline__ void expsum(const uint4& v, float2 negM, float2& s) {
         const float2 l2e = make_float2(1.4426950408889634f, 1.4426950408889634f);
@@ -389,7 +389,7 @@ __device__ void item_A(const StepParams& P, int b, int idx, const ItemRef& nxt, 
                 double x[2];
                 unpack(w[j], x);
                 cm = fmax(cm, fmax(x[0], x[1]));
-                mn = fmin(mn, fmin(x[0], x[1]));
+                mn = fmin_nan(mn, fmin_nan(x[0], x[1]));
             }
             if (cm > m) {
                 if (s != 0.0) s *= exp(m - cm);
@@ -432,8 +432,9 @@ __device__ void item_A(const StepParams& P, int b, int idx, const ItemRef& nxt, 
         }
     }
     as.next_pre = nxt_issued;
-    // -inf logit (require_finite, dist.cpp:27-36); NaN / +inf surface in the sum
-    if (__any_sync(kFull, isinf(mn)) && lane == 0) flag(P, SSV_STATUS_NONFINITE);
+    // -inf or NaN logit (require_finite, dist.cpp:27-36; the running minimum
+    // propagates NaN even where the max and the sum skip it); +inf surfaces in the sum
+    if (__any_sync(kFull, !isfinite(mn)) && lane == 0) flag(P, SSV_STATUS_NONFINITE);
     // Warp fold (fixed order, fp64) -> one partial per warp; no CTA barrier, so
     // the warps of a CTA drift freely between runs.
     double M = (double)m;  // warp-uniform (fp32 path); fp64 storage keeps per-lane maxima
@@ -1294,10 +1295,12 @@ __global__ void __launch_bounds__(NT, 1) k_verify_cluster(StepParams P) {
     int* offs = reinterpret_cast<int*>(zg + 3 * G + 1);                         // [NS]
     int* fills = offs + NS;                                                     // [NS] fills issued per slot - 1
 
-    // Every rank pushes its slice partials into the other ranks' shared memory
-    // before the first full cluster barrier: arrive now, wait (all ranks have
-    // started) just before the row folds.
-    if (EXACT) asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
+    // Every rank pushes its slice partials (exact) or its slice totals (every
+    // variant) into the other ranks' shared memory before the first full
+    // cluster barrier, which needs every CTA of the cluster to have started:
+    // arrive now, wait just before the first push (exact: the row folds;
+    // sigmoid / probabilities: the granule pass).
+    asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
     const bool tr = P.trace && rank == 0 && tid == 0;  // per-row stamps (tools/trace_step.py)
     if (tr) {
         trace(P, 8 * b);
@@ -1488,7 +1491,7 @@ __global__ void __launch_bounds__(NT, 1) k_verify_cluster(StepParams P) {
                 part[r] = pv;
             }
         }
-        if (__any_sync(kFull, isinf(mn)) && lane == 0) flag(P, SSV_STATUS_NONFINITE);
+        if (__any_sync(kFull, !isfinite(mn)) && lane == 0) flag(P, SSV_STATUS_NONFINITE);
         if (tr) trace(P, 8 * b + 1);
         cl.sync();  // slice partials visible to the cluster
         if (tr) trace(P, 8 * b + 2);
@@ -1572,6 +1575,7 @@ __global__ void __launch_bounds__(NT, 1) k_verify_cluster(StepParams P) {
     __syncthreads();
     if (tr) trace(P, 8 * b + 3);
     const Decision d = sh.dec;
+    if (!EXACT) asm volatile("barrier.cluster.wait.aligned;" ::: "memory");  // every rank has started
     // Granule masses of this rank's slice of the needed row(s) (L2-hot re-read),
     // also stored to global for the rare last-positive fallback.  The slice
     // total (fixed order) is pushed into every rank's rtot[rank] so that after
@@ -1871,6 +1875,27 @@ __global__ void k_gen_uniforms(uint64_t seed, int B, int G, int V, double* draft
 
 // ---------------------------------------------------------------------------
 // Host-side launchers.
+//
+// Experiment knobs (SSV_* environment variables) exist only in experiment
+// builds (make EXPERIMENTS=1 -> -DSSV_EXPERIMENTS); the product library always
+// uses the defaults, so no environment variable can change what it computes.
+static int knob(const char* name, int dflt) {
+#ifdef SSV_EXPERIMENTS
+    const char* e = getenv(name);
+    return e ? atoi(e) : dflt;
+#else
+    (void)name;
+    return dflt;
+#endif
+}
+static bool knob_set(const char* name) {
+#ifdef SSV_EXPERIMENTS
+    return getenv(name) != nullptr;
+#else
+    (void)name;
+    return false;
+#endif
+}
 static int sm_count() {
     static int n = 0;
     if (n == 0) {
@@ -1906,13 +1931,10 @@ void plan_geometry(int dtype, int act, StepParams& P) {
         // run ends in a warp fold and a claim, so long runs keep the ring busy
         // (measured: 38-chunk runs stream at ~100% of the copy roofline, 4-chunk
         // runs at ~70%).  The lags below scale with the run length.
-        static const int run_cap = [] {  // experiment knob (SSV_RUNA)
-            const char* e = getenv("SSV_RUNA");
-            return e ? std::max(1, atoi(e)) : 64;
-        }();
+        static const int run_cap = std::max(1, knob("SSV_RUNA", 64));
         long want = ((long)P.Kc * P.B * P.NR + 4 * resident - 1) / (4 * resident);
         want = std::max<long>(1, std::min<long>({want, (long)P.Kc, (long)run_cap}));
-        static const int run_force = getenv("SSV_RUNA_FORCE") ? atoi(getenv("SSV_RUNA_FORCE")) : 0;  // experiment knob
+        static const int run_force = knob("SSV_RUNA_FORCE", 0);
         if (run_force > 0) want = std::min<long>(run_force, P.Kc);
         const long runs = (P.Kc + want - 1) / want;
         P.runA = (int)((P.Kc + runs - 1) / runs);
@@ -1923,7 +1945,7 @@ void plan_geometry(int dtype, int act, StepParams& P) {
     P.nph[IT_D] = P.sample_mode ? 0 : 1;  // exact: row statistics + decision; sigmoid / probs: gathers only
     P.nph[IT_B] = P.nB;
     P.nph[IT_L] = 1;
-    static const bool a_only = getenv("SSV_AONLY") != nullptr;  // experiment knob: A phase alone (no results)
+    static const bool a_only = knob_set("SSV_AONLY");  // experiment builds only: A phase alone (no results)
     if (a_only && exact) P.nph[IT_D] = P.nph[IT_B] = P.nph[IT_L] = 0;
     // Phase offsets, in segments of one batch row each: a phase of row b is
     // dispatched about one resident wave after the phase it waits on, so the
@@ -1931,10 +1953,7 @@ void plan_geometry(int dtype, int act, StepParams& P) {
     // earlier) is still in L2 when its B-items re-read it.
     // items in progress at any time: one per resident CTA plus one claimed ahead
     const long seg = (long)P.nph[0] + P.nph[1] + P.nph[2] + P.nph[3];
-    static const int lag_mult = [] {  // experiment knob (SSV_LAG_MULT), default by run length
-        const char* e = getenv("SSV_LAG_MULT");
-        return e ? std::max(1, atoi(e)) : 0;
-    }();
+    static const int lag_mult = std::max(0, knob("SSV_LAG_MULT", 0));  // 0: default by run length
     const int wave = (int)((2 * resident + seg - 1) / seg);
     // A D-item waits for its row's runs, which take ~runA/8 "waves" of
     // claims to complete; B- and L-items follow one wave after that.
@@ -1988,7 +2007,7 @@ int trace_slots(const StepParams& P) { return 8 * P.B + 26; }
 
 // Programmatic stream serialization for the verify launches (see pdl_enter).
 static int pdl_attr(cudaLaunchAttribute& a) {
-    static const bool off = getenv("SSV_NO_PDL") != nullptr;  // experiment knob
+    static const bool off = knob_set("SSV_NO_PDL");
     if (off) return 0;
     a.id = cudaLaunchAttributeProgrammaticStreamSerialization;
     a.val.programmaticStreamSerializationAllowed = 1;
@@ -2012,7 +2031,7 @@ static void launch_verify_t(const StepParams& P, const Launch& L) {
     const unsigned grid = std::min<unsigned>(P.n_items, (unsigned)(sm_count() * per_sm));
     StepParams Q = P;
     Q.claim_ahead = P.n_items > 2u * grid;
-    static const int dbgm = getenv("SSV_DBG_MODE") ? atoi(getenv("SSV_DBG_MODE")) : 0;
+    static const int dbgm = knob("SSV_DBG_MODE", 0);
     Q.dbg = dbgm;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid, 1, 1);
@@ -2079,16 +2098,16 @@ static int max_active_clusters(int cs, int smem) {
 // which B fit on the GPU together.
 template <typename T, int ACT>
 static bool plan_cluster_t(StepParams& P, int s, bool allow_resident) {
-    static const bool off = getenv("SSV_NO_CLUSTER") != nullptr;  // experiment knob
-    static const bool dbg = getenv("SSV_DEBUG") != nullptr;
+    static const bool off = knob_set("SSV_NO_CLUSTER");
+    static const bool dbg = knob_set("SSV_DEBUG");
     if (off || P.sample_mode || P.G > 256) return false;
     const int NRc = ACT == ACT_SOFTMAX ? 2 * P.G + (P.NR > 2 * P.G ? 1 : 0) : 0;  // bonus stats only if materialized
     if (NRc > kMaxRowsSmem) return false;  // the decision reads every row's statistics from SMEM
     // (two-CTA clusters measured slower than the streaming kernel at B = 64)
-    static const int res_env = getenv("SSV_RES_MODE") ? atoi(getenv("SSV_RES_MODE")) : 2;  // experiment knob
+    static const int res_env = knob("SSV_RES_MODE", 2);
     const int res_mode = allow_resident ? res_env : 0;
-    static const int force_cs = getenv("SSV_FORCE_CS") ? atoi(getenv("SSV_FORCE_CS")) : 0;  // experiment knob
-    static const bool res_nopad = getenv("SSV_RES_NOPAD") != nullptr;  // experiment knob
+    static const int force_cs = knob("SSV_FORCE_CS", 0);
+    static const bool res_nopad = knob_set("SSV_RES_NOPAD");
     for (int pass = res_mode == 2 ? 0 : 1; pass < 2; ++pass)
     for (int cs : {16, 12, 11, 10, 9, 8, 4}) {
         if (force_cs && cs != force_cs) continue;
@@ -2125,7 +2144,7 @@ static bool plan_cluster_t(StepParams& P, int s, bool allow_resident) {
                     P.cl_threads = nt;
                     P.cl_pieces = 1;
                     P.cl_pe = SE;
-                    static const int dbgm = getenv("SSV_DBG_MODE") ? atoi(getenv("SSV_DBG_MODE")) : 0;
+                    static const int dbgm = knob("SSV_DBG_MODE", 0);
                     P.dbg = dbgm;  // experiment bits (4: no bonus-row prefetch)
                     P.NR = NRc;
                     return true;
@@ -2153,9 +2172,9 @@ static bool plan_cluster_t(StepParams& P, int s, bool allow_resident) {
         // shapes stay on the streaming kernel, 6-60 % faster there).
         // pieces of >= 12 KB (measured: 12 KB beats 16 KB on every ring shape,
         // e.g. B=64 gamma=8 V=51865 bf16 67.0 -> 59.6 us; 10 KB loses C3 f32)
-        static const int piece_min = getenv("SSV_PIECE_KB") ? atoi(getenv("SSV_PIECE_KB")) * 1024 : 12288;  // experiment knob
+        static const int piece_min = knob("SSV_PIECE_KB", 12) * 1024;
         const bool pieced = NS < NRc && SE * s >= 2 * piece_min;
-        static const bool no_gate = getenv("SSV_NO_GATE") != nullptr;  // experiment knob
+        static const bool no_gate = knob_set("SSV_NO_GATE");
         if (!no_gate && !(cta_bytes <= 300L * 1024 || (NS >= 4 && cta_bytes <= 600L * 1024) || (P.B >= 48 && cta_bytes <= 520L * 1024) ||
                           (P.B >= 32 && P.V <= 65536 && cta_bytes <= 600L * 1024 && (NS >= 3 || pieced))))
             continue;
@@ -2163,7 +2182,7 @@ static bool plan_cluster_t(StepParams& P, int s, bool allow_resident) {
         // a slot is refilled after a piece's fold, not a whole slice's
         // (C3 f32, 32 KB slices in 16 KB pieces: 48.4 -> 44.7 us; 8 KB pieces
         // measured slower than whole 16 KB slices).
-        static const int pieces_env = getenv("SSV_PIECES") ? atoi(getenv("SSV_PIECES")) : 0;  // experiment knob
+        static const int pieces_env = knob("SSV_PIECES", 0);
         int H = 1, PE = SE, NSu = NS;
         const int want_h = pieces_env > 0 ? pieces_env : std::max(1, std::min(4, SE * s / piece_min));
         if (NS < NRc && want_h > 1) {
@@ -2191,7 +2210,7 @@ static bool plan_cluster_t(StepParams& P, int s, bool allow_resident) {
         P.cl_threads = kClThreads;
         P.cl_pieces = H;
         P.cl_pe = PE;
-        static const int dbgm = getenv("SSV_DBG_MODE") ? atoi(getenv("SSV_DBG_MODE")) : 0;
+        static const int dbgm = knob("SSV_DBG_MODE", 0);
         P.dbg = dbgm;
         if (ACT == ACT_SOFTMAX) P.NR = NRc;  // rowstat rows the cluster path writes
         return true;

@@ -248,9 +248,36 @@ class Verifier:
         return buf
 
     # ---------------- device entry points (torch CUDA tensors) ----------------
+    @staticmethod
+    def _check_device_args(what, z_p, z_q, ids, u):
+        """The C-ABI takes raw pointers with a row pitch of V: reject what it
+        would misread (the reference's validate() rejects shape errors the
+        same way, verify_reference.cpp:12-21)."""
+        import torch
+
+        for name, t in (("z_p", z_p), ("z_q", z_q), ("draft_tokens", ids), ("uniforms", u)):
+            if not isinstance(t, torch.Tensor) or not t.is_cuda:
+                raise SsvInvalidArgument(f"{what}: {name} must be a CUDA tensor")
+            if not t.is_contiguous():
+                raise SsvInvalidArgument(f"{what}: {name} must be contiguous (row pitch = V)")
+            if t.device != z_q.device:
+                raise SsvInvalidArgument(f"{what}: {name} is on {t.device}, z_q on {z_q.device}")
+        if z_q.dim() != 3 or z_p.dim() != 3:
+            raise SsvInvalidArgument(f"{what}: z_p and z_q must be [B, steps, V]")
+        B, gamma, V = z_q.shape
+        if z_p.shape[0] != B or z_p.shape[2] != V or z_p.shape[1] not in (gamma, gamma + 1):
+            raise SsvInvalidArgument(f"{what}: StepInputs: p must be B x gamma(+1) x V matching q")
+        if z_p.dtype != z_q.dtype:
+            raise SsvInvalidArgument(f"{what}: z_p ({z_p.dtype}) and z_q ({z_q.dtype}) differ in dtype")
+        if ids.dtype != torch.int32 or tuple(ids.shape) != (B, gamma):
+            raise SsvInvalidArgument(f"{what}: draft_tokens must be int32 [B, gamma]")
+        if u.dtype != torch.float64 or tuple(u.shape) != (B, gamma + 1):
+            raise SsvInvalidArgument(f"{what}: uniforms must be float64 [B, gamma + 1]")
+
     def _device_call(self, fn, what, z_p, z_q, ids, u, alpha, beta, flags, out):
         import torch
 
+        self._check_device_args(what, z_p, z_q, ids, u)
         self._bind_torch_stream()
         B, gamma, V = z_q.shape
         a = Args(B, gamma, V, z_p.shape[1], _dtype_code(z_q.dtype), z_p.data_ptr(), z_q.data_ptr(),
@@ -395,14 +422,26 @@ class Verifier:
 
     # ---------------- pinned host memory ----------------
     def host_empty(self, shape, dtype) -> np.ndarray:
-        """numpy array in pinned memory (freed with the Verifier's library)."""
+        """numpy array in pinned memory; the pages are released (ssv_host_free)
+        when the last array viewing them is garbage-collected."""
         dt = np.dtype(dtype)
         n = int(np.prod(shape)) * dt.itemsize
         ptr = self.lib.ssv_host_alloc(max(n, 1))
         if not ptr:
             raise SsvError("ssv_host_alloc failed")
         buf = (C.c_char * max(n, 1)).from_address(ptr)
-        arr = np.frombuffer(buf, dtype=dt, count=int(np.prod(shape))).reshape(shape)
-        self._pinned = getattr(self, "_pinned", [])
-        self._pinned.append(ptr)
-        return arr
+        buf._owner = _PinnedPages(self.lib, ptr)  # lives as long as the buffer numpy views
+        return np.frombuffer(buf, dtype=dt, count=int(np.prod(shape))).reshape(shape)
+
+
+class _PinnedPages:
+    """Owner of one ssv_host_alloc block (freed with the last view of it)."""
+
+    def __init__(self, lib, ptr):
+        self.lib, self.ptr = lib, ptr
+
+    def __del__(self):
+        try:
+            self.lib.ssv_host_free(C.c_void_p(self.ptr))
+        except Exception:
+            pass
