@@ -98,6 +98,14 @@ void* ssv_get_stream(const ssv_ctx* ctx);
 const char* ssv_last_error(const ssv_ctx* ctx);
 /* Number of kernels the last verify/sample/generate call launched. */
 int ssv_last_launch_count(const ssv_ctx* ctx);
+/* The plan the last verify call launched: info[0] = SSV_PLAN_*, then cluster
+ * size, threads per CTA, shared-memory slots, statistics rows per cluster,
+ * pieces per row slice (the first n of these).  Diagnostics for tests and the
+ * bench; no reference counterpart (the reference has one CPU code path). */
+#define SSV_PLAN_STREAMING 0
+#define SSV_PLAN_CLUSTER_RESIDENT 1
+#define SSV_PLAN_CLUSTER_RING 2
+int ssv_last_plan(const ssv_ctx* ctx, int32_t* info, int32_t n);
 
 /* Kernel selection for the verify entry points: AUTO
  * picks the cluster kernel when every batch row can get a resident thread-

@@ -242,25 +242,59 @@ inline Staged stage(std::span<const double> x, Storage s) {
     return out;
 }
 
-template <typename Fn>
-VerificationResult run(Fn fn, ssv_ctx* ctx, const Grid3& zp, const Grid3& zq, const Matrix<int32_t>& ids,
-                       const Matrix<double>& u, Storage s, double alpha, double beta, uint32_t flags = 0,
-                       void* residual = nullptr) {
-    const size_t B = zq.batch(), G = zq.steps(), V = zq.vocab();
-    if (zp.batch() != B || zp.vocab() != V || (zp.steps() != G && zp.steps() != G + 1))
-        throw std::invalid_argument("StepInputs: p must be B x gamma(+1) x V matching q");
-    if (ids.rows() != B || ids.cols() != G) throw std::invalid_argument("StepInputs: draft_tokens must be B x gamma");
-    if (u.rows() != B || u.cols() != G + 1) throw std::invalid_argument("StepInputs: uniforms must be B x (gamma+1)");
+// Pointer to a row-major matrix's storage (ssv::Matrix or the reference's
+// specsamp::Matrix, whose rows are contiguous).
+template <typename M>
+auto mat_ptr(const M& m) -> decltype(m.row(0).data()) {
+    return m.rows() && m.cols() ? m.row(0).data() : nullptr;
+}
+
+// Shape checks with the reference's messages: StepInputs::validate
+// (verify_reference.cpp:12-21) or SigmoidStepInputs::validate
+// (verify_sigmoid.cpp:14-23).
+template <typename G, typename MI, typename MU>
+void check_shapes(const G& zp, const G& zq, const MI& ids, const MU& u, bool sigmoid) {
+    const size_t B = zq.batch(), Gm = zq.steps(), V = zq.vocab();
+    if (zp.batch() != B || zp.vocab() != V || (zp.steps() != Gm && zp.steps() != Gm + 1))
+        throw std::invalid_argument(sigmoid ? "SigmoidStepInputs: z_p must be B x gamma(+1) x V matching z_q"
+                                            : "StepInputs: p must be B x gamma(+1) x V matching q");
+    if (ids.rows() != B || ids.cols() != Gm)
+        throw std::invalid_argument(sigmoid ? "SigmoidStepInputs: draft_tokens must be B x gamma"
+                                            : "StepInputs: draft_tokens must be B x gamma");
+    if (u.rows() != B || u.cols() != Gm + 1)
+        throw std::invalid_argument(sigmoid ? "SigmoidStepInputs: uniforms must be B x (gamma+1)"
+                                            : "StepInputs: uniforms must be B x (gamma+1)");
+}
+
+// The uniform range check of StepInputs::validate (verify_reference.cpp:28-33),
+// which the sigmoid SEQUENTIAL oracle inherits through verify_sequential
+// (verify_sigmoid.cpp:50-58) and the fused sigmoid path does not.
+template <typename MU>
+void check_uniforms(const MU& u) {
+    for (size_t r = 0; r < u.rows(); ++r)
+        for (size_t c = 0; c < u.cols(); ++c) {
+            const double x = u(r, c);
+            if (!(x >= 0.0) || !(x < 1.0)) throw std::invalid_argument("StepInputs: uniforms must lie in [0, 1)");
+        }
+}
+
+// One host-entry call (ssv_verify_*_host): stage the double grids in the
+// storage type, run on the device, results into a VerificationResult.  G is
+// ssv::Grid3 or specsamp::Grid3; MI / MU ssv:: or specsamp::Matrix.
+template <typename Fn, typename G, typename MI, typename MU>
+VerificationResult run(Fn fn, ssv_ctx* ctx, const G& zp, const G& zq, const MI& ids, const MU& u, Storage s,
+                       double alpha, double beta, uint32_t flags = 0, void* residual = nullptr) {
+    const size_t B = zq.batch(), Gm = zq.steps(), V = zq.vocab();
     const Staged sp = stage(zp.flat(), s), sq = stage(zq.flat(), s);
     VerificationResult r;
     r.accepted_len.assign(B, 0);
-    r.tau = Matrix<double>(B, G);
+    r.tau = Matrix<double>(B, Gm);
     r.final_token.assign(B, kNoToken);
     r.resample_used.assign(B, 0);
     r.residual_denom.assign(B, 0.0);
-    ssv_verify_args a{static_cast<int32_t>(B), static_cast<int32_t>(G), static_cast<int32_t>(V),
-                      static_cast<int32_t>(zp.steps()), static_cast<int32_t>(s), sp.ptr, sq.ptr, ids.data(), u.data(),
-                      alpha, beta, flags};
+    ssv_verify_args a{static_cast<int32_t>(B), static_cast<int32_t>(Gm), static_cast<int32_t>(V),
+                      static_cast<int32_t>(zp.steps()), static_cast<int32_t>(s), sp.ptr, sq.ptr, mat_ptr(ids),
+                      mat_ptr(u), alpha, beta, flags};
     ssv_verify_out o{r.accepted_len.data(), r.final_token.data(), r.resample_used.data(), r.tau.data(),
                      r.residual_denom.data(), nullptr, nullptr, residual, nullptr};
     check(ctx, fn(ctx, &a, &o));
@@ -284,24 +318,29 @@ inline MemoryTrace analytic_trace(const VerificationResult& r, size_t B, size_t 
 }  // namespace detail
 
 // ---- drop-ins ----------------------------------------------------------------
-// materialize_softmax_into(z_p), (z_q) + verify_sequential, logits in.
+// materialize_softmax_into(z_p), (z_q) + verify_sequential, logits in
+// (bench.cpp:113-127, decode.cpp:121-135).
 inline VerificationResult verify_exact(const LogitStepInputs& in, Storage storage = Storage::f32,
                                        Device& dev = default_device()) {
+    detail::check_shapes(in.z_p, in.z_q, in.draft_tokens, in.uniforms, false);
     return detail::run(ssv_verify_exact_host, dev.get(), in.z_p, in.z_q, in.draft_tokens, in.uniforms, storage, 0, 0);
 }
 
 // verify_reference.hpp:12 -- probabilities in, fp64 storage (the reference's own type).
 inline VerificationResult verify_sequential(const StepInputs& in, Device& dev = default_device()) {
+    detail::check_shapes(in.p.values, in.q.values, in.draft_tokens, in.uniforms, false);
     return detail::run(ssv_verify_probs_host, dev.get(), in.p.values, in.q.values, in.draft_tokens, in.uniforms,
                        Storage::f64, 0, 0);
 }
 
 // verify_fused.hpp:24-27 -- same signature; like the reference, q is consumed:
-// the clamped residual max(0, p - q) is written back into it.  `workers` and
-// the tile plan shape only the analytic MemoryTrace.
+// the clamped residual max(0, p - q) of every drafted row is written back into
+// it (verify_fused.cpp:50).  `workers` and the tile plan shape only the
+// analytic MemoryTrace (the device picks its own tiling).
 inline FusedVerifyOutput verify_fused(StepInputs& in, const TilePlan& plan, unsigned workers,
                                       Device& dev = default_device()) {
     (void)workers;
+    detail::check_shapes(in.p.values, in.q.values, in.draft_tokens, in.uniforms, false);
     if (plan.vocab_size != in.vocab() || plan.tiles.empty())
         throw std::invalid_argument("verify_fused: tile plan does not match the input vocabulary");
     std::vector<double> residual(in.q.values.size());
@@ -313,21 +352,30 @@ inline FusedVerifyOutput verify_fused(StepInputs& in, const TilePlan& plan, unsi
     return out;
 }
 
-// verify_sigmoid.hpp:41 / 48-51.
+// verify_sigmoid.hpp:41.  Like the reference, the sequential oracle rejects
+// uniforms outside [0, 1) (it validates through verify_sequential,
+// verify_sigmoid.cpp:50-58 -> verify_reference.cpp:28-33).
 inline VerificationResult verify_sigmoid_sequential(const SigmoidStepInputs& in, Storage storage = Storage::f32,
                                                     Device& dev = default_device()) {
     in.bounds.validate();
+    detail::check_shapes(in.z_p, in.z_q, in.draft_tokens, in.uniforms, true);
+    detail::check_uniforms(in.uniforms);
     return detail::run(ssv_verify_sigmoid_host, dev.get(), in.z_p, in.z_q, in.draft_tokens, in.uniforms, storage,
                        in.bounds.alpha, in.bounds.beta, in.emulate_half ? SSV_EMULATE_HALF : 0u);
 }
 
+// verify_sigmoid.hpp:48-51.  Inputs untouched; uniforms not range-checked
+// (SigmoidStepInputs::validate, verify_sigmoid.cpp:13-33).
 inline FusedVerifyOutput verify_sigmoid_fused(const SigmoidStepInputs& in, const TilePlan& plan, unsigned workers,
                                               Storage storage = Storage::f32, Device& dev = default_device()) {
     (void)workers;
+    in.bounds.validate();
+    detail::check_shapes(in.z_p, in.z_q, in.draft_tokens, in.uniforms, true);
     if (plan.vocab_size != in.vocab() || plan.tiles.empty())
         throw std::invalid_argument("verify_sigmoid_fused: tile plan does not match the vocabulary");
     FusedVerifyOutput out;
-    out.result = verify_sigmoid_sequential(in, storage, dev);
+    out.result = detail::run(ssv_verify_sigmoid_host, dev.get(), in.z_p, in.z_q, in.draft_tokens, in.uniforms,
+                             storage, in.bounds.alpha, in.bounds.beta, in.emulate_half ? SSV_EMULATE_HALF : 0u);
     out.trace = detail::analytic_trace(out.result, in.batch(), in.gamma(), in.vocab(), plan);
     return out;
 }

@@ -37,6 +37,7 @@ struct ssv_ctx {
     ProfileHook prof;
     bool profiling = false;
     int path = SSV_PATH_AUTO;
+    int32_t plan[6] = {0, 0, 0, 0, 0, 0};  // ssv_last_plan
     unsigned long long* trace = nullptr;  // diagnostics (ssv_debug_trace)
     int trace_cap = 0;
     uint32_t* status_mirror = nullptr;    // set by run_host for the duration of its launch
@@ -207,6 +208,14 @@ int run_device(ssv_ctx* ctx, int variant, const ssv_verify_args* a, ssv_verify_o
     P.status_mirror = ctx->status_mirror;
     P.trace = (ctx->trace && trace_slots(P) <= ctx->trace_cap) ? ctx->trace : nullptr;
     ctx->launches = 0;
+    // kernel, cluster size, threads, slots, rows, pieces (ssv_last_plan)
+    ctx->plan[0] = P.cl_size > 0 ? (P.cl_resident ? SSV_PLAN_CLUSTER_RESIDENT : SSV_PLAN_CLUSTER_RING)
+                                 : SSV_PLAN_STREAMING;
+    ctx->plan[1] = P.cl_size;
+    ctx->plan[2] = P.cl_size > 0 ? P.cl_threads : kCtaThreads;
+    ctx->plan[3] = P.cl_slots;
+    ctx->plan[4] = P.cl_rows;
+    ctx->plan[5] = P.cl_pieces;
     launch_verify(a->dtype, act, P, want_p ? o->p : nullptr, (a->flags & SSV_WANT_Q) ? o->q : nullptr,
                   (a->flags & SSV_WANT_RESIDUAL) ? o->residual : nullptr, ctx->launcher());
     CK(cudaGetLastError());
@@ -425,6 +434,12 @@ void* ssv_get_stream(const ssv_ctx* ctx) { return ctx ? static_cast<void*>(ctx->
 const char* ssv_last_error(const ssv_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
 
 int ssv_last_launch_count(const ssv_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+int ssv_last_plan(const ssv_ctx* ctx, int32_t* info, int32_t n) {
+    if (!ctx || !info || n < 1) return SSV_EINVAL;
+    for (int i = 0; i < n && i < 6; ++i) info[i] = ctx->plan[i];
+    return SSV_OK;
+}
 
 int ssv_set_path(ssv_ctx* ctx, int32_t path) {
     if (!ctx) return SSV_EINVAL;

@@ -103,6 +103,26 @@ __device__ __forceinline__ float exp_rel(float x, float m) {
 }
 __device__ __forceinline__ double exp_rel(double x, double m) { return exp(x - m); }
 
+// e^(x - m) to ~3e-7 relative for the materialized p / q / residual grids
+// (north star: 1e-5 relative, and residual elements where p ~ q cancel need
+// both terms far more accurate than exp_rel's ~2e-6 at |x - m| ~ 40): the
+// difference as an exact float pair (TwoSum), times log2(e) as hi + lo, then
+// 2^n * 2^f with |f| <= 0.5 from MUFU ex2.
+__device__ __forceinline__ float exp_rel_acc(float x, float m) {
+    const float s = x - m;
+    const float bv = s - x;
+    const float e = (x - (s - bv)) + (-m - bv);
+    constexpr float L = 1.44269502162933349609375f;  // log2(e), fp32 head
+    constexpr float Ll = 1.925962991126617468e-8f;   // log2(e) - L
+    const float yh = s * L;
+    const float yl = fmaf(s, L, -yh) + fmaf(s, Ll, e * L);
+    const float n = rintf(yh);
+    float r;
+    asm("ex2.approx.f32 %0, %1;" : "=f"(r) : "f"((yh - n) + yl));
+    return scalbnf(r, (int)n);
+}
+__device__ __forceinline__ double exp_rel_acc(double x, double m) { return exp(x - m); }
+
 // dist.cpp:17-23 stable_sigmoid, fp64 (exact path).
 __device__ __forceinline__ double stable_sigmoid_d(double t) {
     if (t >= 0.0) return 1.0 / (1.0 + exp(-t));

@@ -1769,42 +1769,58 @@ __global__ void __launch_bounds__(NT, 1) k_verify_cluster(StepParams P) {
 
 // ---------------------------------------------------------------------------
 // K3: optional materialized grids (activation.cpp:20-49; verify_fused.cpp:50
-// residual-in-q semantics; verify_sigmoid.cpp:39-48).
+// residual-in-q semantics; verify_sigmoid.cpp:39-48), after the verify launch
+// that produced the row statistics (a normalized softmax row cannot be written
+// before its row's statistics exist, so this is a second pass over the logits;
+// it reads every logit once and writes each requested grid once).
+// Work unit = (row, 4096-element segment): a drafted pair (b, c < gamma)
+// writes p, q and residual from one read of both rows; the bonus row (b, gamma)
+// writes p.  Row-major addressing (no per-element division), coalesced
+// element loads (rows of odd V start at any alignment).  Values: fp32 via
+// exp_rel_acc (~3e-7) / sigmoid_fast, fp64 storage in fp64.
+constexpr int kMatSeg = 4096;
 template <typename T, int ACT>
 __global__ void __launch_bounds__(kThreads) k_materialize(StepParams P, void* outp, void* outq, void* outr) {
     using A = typename Elem<T>::acc;
     using O = typename std::conditional<sizeof(A) == 8, double, float>::type;
-    const size_t V = (size_t)P.V;
-    const size_t np = (size_t)P.B * P.PS * V, nq = (size_t)P.B * P.G * V;
+    const int V = P.V, G = P.G;
+    const int nseg = (V + kMatSeg - 1) / kMatSeg;
+    const int pairs = P.B * G, bonus = P.PS == G + 1 && outp ? P.B : 0;
+    const long units = (long)(pairs + bonus) * nseg;
     const A alpha = (A)P.alpha, invw = (A)(1.0 / P.width);
-    auto act = [&](A x, const double2& st) -> A {
-        if (ACT == ACT_SOFTMAX) return exp_rel(x, (A)st.x) * (A)(1.0 / st.y);
-        if (is_sigmoid(ACT)) return ACT == ACT_SIGMOID_HALF ? (A)sigmoid_act<ACT>(P, (double)x) : sigmoid_fast((x - alpha) * invw);
-        return x;
-    };
-    auto stat_of = [&](int b, int r) -> double2 {
-        if (ACT != ACT_SOFTMAX) return make_double2(0.0, 1.0);
-        return P.rowstat[(size_t)b * P.NR + r];
-    };
-    const size_t stride = (size_t)gridDim.x * blockDim.x;
-    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < np; i += stride) {
-        const size_t rowi = i / V;
-        const int b = (int)(rowi / P.PS), c = (int)(rowi % P.PS);
-        const A x = load_elem(reinterpret_cast<const T*>(P.zp) + i);
-        const A pv = act(x, stat_of(b, c < P.G ? c : 2 * P.G));
-        if (outp) reinterpret_cast<O*>(outp)[i] = (O)pv;
-    }
-    if (!outq && !outr) return;
-    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < nq; i += stride) {
-        const size_t rowi = i / V, e = i % V;
-        const int b = (int)(rowi / P.G), c = (int)(rowi % P.G);
-        const A xq = load_elem(reinterpret_cast<const T*>(P.zq) + i);
-        const A qv = act(xq, stat_of(b, P.G + c));
-        if (outq) reinterpret_cast<O*>(outq)[i] = (O)qv;
-        if (outr) {
-            const A xp = load_elem(p_row<T>(P, b, c) + e);
-            const A pv = act(xp, stat_of(b, c));
-            reinterpret_cast<O*>(outr)[i] = (O)(pv - qv > (A)0 ? pv - qv : (A)0);
+    const bool want_q = outq || outr;
+    for (long w = blockIdx.x; w < units; w += gridDim.x) {
+        const int row = (int)(w / nseg), seg = (int)(w - (long)row * nseg);
+        const bool is_pair = row < pairs;
+        const int b = is_pair ? row / G : row - pairs;
+        const int c = is_pair ? row - b * G : G;
+        const int lo = seg * kMatSeg, hi = min(V, lo + kMatSeg);
+        double2 sp = make_double2(0.0, 1.0), sq = sp;
+        if (ACT == ACT_SOFTMAX) {
+            sp = __ldcg(&P.rowstat[(size_t)b * P.NR + (is_pair ? c : 2 * G)]);
+            if (is_pair && want_q) sq = __ldcg(&P.rowstat[(size_t)b * P.NR + G + c]);
+        }
+        const A Mp = (A)sp.x, iSp = (A)(1.0 / sp.y), Mq = (A)sq.x, iSq = (A)(1.0 / sq.y);
+        auto act = [&](A x, A M, A iS) -> A {
+            if (ACT == ACT_SOFTMAX) return exp_rel_acc(x, M) * iS;
+            if (ACT == ACT_SIGMOID_HALF) return (A)sigmoid_act<ACT>(P, (double)x);
+            if (is_sigmoid(ACT)) return sigmoid_fast((x - alpha) * invw);
+            return x;
+        };
+        const T* pr = p_row<T>(P, b, c);
+        const T* qr = is_pair ? q_row<T>(P, b, c) : nullptr;
+        O* op = outp ? reinterpret_cast<O*>(outp) + ((size_t)b * P.PS + c) * (size_t)V : nullptr;
+        O* oq = (outq && is_pair) ? reinterpret_cast<O*>(outq) + ((size_t)b * G + c) * (size_t)V : nullptr;
+        O* orr = (outr && is_pair) ? reinterpret_cast<O*>(outr) + ((size_t)b * G + c) * (size_t)V : nullptr;
+        for (int i = lo + threadIdx.x; i < hi; i += kThreads) {
+            const bool need_p = op || orr;
+            const A pv = need_p ? act(load_elem(pr + i), Mp, iSp) : (A)0;
+            if (op) op[i] = (O)pv;
+            if (is_pair && want_q) {
+                const A qv = act(load_elem(qr + i), Mq, iSq);
+                if (oq) oq[i] = (O)qv;
+                if (orr) orr[i] = (O)(pv - qv > (A)0 ? pv - qv : (A)0);
+            }
         }
     }
 }
@@ -2143,6 +2159,7 @@ static bool plan_cluster_t(StepParams& P, int s, bool allow_resident) {
                     P.cl_smem = smem1;
                     P.cl_threads = nt;
                     P.cl_pieces = 1;
+                    P.cl_resident = 1;
                     P.cl_pe = SE;
                     static const int dbgm = knob("SSV_DBG_MODE", 0);
                     P.dbg = dbgm;  // experiment bits (4: no bonus-row prefetch)
@@ -2209,6 +2226,7 @@ static bool plan_cluster_t(StepParams& P, int s, bool allow_resident) {
         P.cl_smem = smem;
         P.cl_threads = kClThreads;
         P.cl_pieces = H;
+        P.cl_resident = 0;
         P.cl_pe = PE;
         static const int dbgm = knob("SSV_DBG_MODE", 0);
         P.dbg = dbgm;
@@ -2264,7 +2282,7 @@ static void launch_cluster_t(const StepParams& P, const Launch& L) {
 template <typename T, int ACT>
 static void launch_mat_t(const StepParams& P, void* p, void* q, void* r, const Launch& L) {
     const int h = L.begin(KID_MATERIALIZE);
-    k_materialize<T, ACT><<<sm_count() * 8, kThreads, 0, L.st>>>(P, p, q, r);
+    k_materialize<T, ACT><<<sm_count() * 8, kThreads, 0, L.st>>>(P, p, q, r);  // grid-stride over units
     L.end(h);
 }
 

@@ -76,6 +76,7 @@ struct StepParams {
     // row it needs in its shared memory.
     int cl_size, cl_se, cl_gps, cl_rows, cl_slots, cl_rowbytes, cl_smem;
     int cl_threads;  // 256, or 512 for all-resident slices with more rows than 8 warps
+    int cl_resident;  // 1: the resident plan (every row slice in shared memory), 0: the ring plan
     int cl_pieces, cl_pe;  // ring units: each row slice in cl_pieces pieces of cl_pe elements
     int dbg;  // experiment bits (SSV_DBG_MODE), 0 in production
     double alpha, width;

@@ -90,6 +90,7 @@ def load_library() -> C.CDLL:
         L.ssv_last_error.restype = C.c_char_p
         L.ssv_last_launch_count.argtypes = [vp]
         L.ssv_set_path.argtypes = [vp, i32]
+        L.ssv_last_plan.argtypes = [vp, C.POINTER(i32), i32]
         for name in ("exact", "sigmoid", "probs", "exact_host", "sigmoid_host", "probs_host"):
             f = getattr(L, "ssv_verify_" + name)
             f.argtypes = [vp, C.POINTER(Args), C.POINTER(Out)]
@@ -115,7 +116,7 @@ EXPORTS = (
     "ssv_verify_probs", "ssv_verify_exact_host", "ssv_verify_sigmoid_host", "ssv_verify_probs_host",
     "ssv_host_alloc", "ssv_host_free", "ssv_sample_softmax", "ssv_make_bench_inputs",
     "ssv_profile_enable", "ssv_profile_disable", "ssv_profile_reset", "ssv_profile_read",
-    "ssv_debug_trace", "ssv_set_path",
+    "ssv_debug_trace", "ssv_set_path", "ssv_last_plan",
 )
 
 KID_VERIFY, KID_MATERIALIZE, KID_GEN = 0, 2, 3
@@ -214,6 +215,15 @@ class Verifier:
     @property
     def last_launch_count(self) -> int:
         return self.lib.ssv_last_launch_count(self.ctx)
+
+    @property
+    def last_plan(self) -> dict:
+        """The plan the last verify call launched (ssv_last_plan)."""
+        info = (C.c_int32 * 6)()
+        self._check(self.lib.ssv_last_plan(self.ctx, info, 6), "ssv_last_plan")
+        kind = {0: "streaming", 1: "cluster_resident", 2: "cluster_ring"}[info[0]]
+        return {"kernel": kind, "cluster_size": info[1], "threads": info[2], "slots": info[3], "rows": info[4],
+                "pieces": info[5]}
 
     def _check(self, rc: int, what: str):
         if rc == SSV_OK:

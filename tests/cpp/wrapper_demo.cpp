@@ -1,6 +1,8 @@
 // Exercises the reference-typed C++ drop-in (include/ssv/ssv.hpp) on the
 // SPEC.md worked examples.  Compiled by tests/test_abi.py on any host; run by
-// tests/test_gpu_misc.py on the GPU.  Exit 0 = all checks passed.
+// tests/test_gpu_cpp.py on the GPU (which also runs tests/cpp/ref_backend.cpp,
+// the same drop-in checked against the reference's own backends).  Exit 0 =
+// all checks passed.
 #include <cmath>
 #include <cstdio>
 #include <stdexcept>
@@ -58,6 +60,57 @@ int main() {
     li.uniforms = ssv::Matrix<double>(1, 2, 0.5);
     const auto re = ssv::verify_exact(li, ssv::Storage::f64);
     EXPECT(re.accepted_len[0] == 1 && re.tau(0, 0) == 1.0 && re.final_token[0] == 1);
+
+    // plan_tiles (tile.cpp:11-23; SPEC.md:184 KAT) and the analytic trace of
+    // verify_fused (tile.cpp:73-100 counting rules): B*gamma*V reads of each
+    // grid, one invocation per (b, c, tile), writes a + partial + tau + resample
+    {
+        const auto plan = ssv::plan_tiles(50257, 1024);
+        EXPECT(plan.tile_count() == 50 && plan.tiles.back().size() == 81 && plan.tiles[1].begin == 1024);
+        ssv::StepInputs big;
+        const size_t B = 2, G = 3, V = 2500;
+        big.p = ssv::ProbTensor(B, G + 1, V);
+        big.q = ssv::ProbTensor(B, G, V);
+        for (size_t b = 0; b < B; ++b)
+            for (size_t c = 0; c <= G; ++c)
+                for (size_t i = 0; i < V; ++i) {
+                    big.p.row(b, c)[i] = (1.0 + (double)((i * 7 + c) % 13)) / (7.0 * V);
+                    if (c < G) big.q.row(b, c)[i] = (1.0 + (double)((i * 5 + b) % 11)) / (6.0 * V);
+                }
+        big.draft_tokens = ssv::Matrix<int32_t>(B, G, 17);
+        big.uniforms = ssv::Matrix<double>(B, G + 1, 0.999);
+        const ssv::StepInputs keep = big;
+        const auto tp = ssv::plan_tiles(V, 1024);
+        const auto fo = ssv::verify_fused(big, tp, 4);
+        EXPECT(fo.trace.hbm_elem_reads_p == B * G * V && fo.trace.hbm_elem_reads_q == B * G * V);
+        EXPECT(fo.trace.kernel_invocations == B * G * 3);
+        uint64_t writes = B * G * V + B * G * 3 + B * G;
+        for (size_t b = 0; b < B; ++b)
+            if (fo.result.resample_used[b] && fo.result.residual_denom[b] > 0.0) writes += V;
+        EXPECT(fo.trace.hbm_elem_writes == writes && fo.trace.peak_tile_bytes == (2 * 1024 + 1024) * 8);
+        for (size_t b = 0; b < B; ++b)  // the residual max(0, p - q) replaced q (verify_fused.cpp:50)
+            for (size_t c = 0; c < G; ++c)
+                for (size_t i = 0; i < V; ++i)
+                    EXPECT(big.q.row(b, c)[i] == std::max(0.0, keep.p.row(b, c)[i] - keep.q.row(b, c)[i]));
+        EXPECT(fo.result == ssv::verify_sequential(keep));
+    }
+
+    // the sigmoid SEQUENTIAL entry point range-checks uniforms like the
+    // reference (verify_sigmoid.cpp:50-58 -> verify_reference.cpp:28-33); the
+    // fused one does not (SigmoidStepInputs::validate)
+    {
+        ssv::SigmoidStepInputs bad = s;
+        bad.uniforms(0, 0) = 1.0;
+        bool t1 = false;
+        try {
+            ssv::verify_sigmoid_sequential(bad);
+        } catch (const std::invalid_argument&) {
+            t1 = true;
+        }
+        EXPECT(t1);
+        const auto fused = ssv::verify_sigmoid_fused(bad, ssv::plan_tiles(2, 1024), 1);
+        EXPECT(fused.result.accepted_len[0] == 0);  // u = 1 > tau: rejected, no throw
+    }
 
     // error behaviour: std::invalid_argument, as the reference's validate()
     bool threw = false;

@@ -90,3 +90,54 @@ def compare(o, g, zp, zq, ids, u, kind, alpha=-1e3, beta=1e3, label=""):
             assert ok, f"{label}: b={b} token {g.final_token[b]} vs oracle {o.final_token[b]} unexplained"
             explained += 1
     return explained
+
+
+# --------------------------------------------------------------------------- campaign helpers
+PARITY_LOG = []  # (label, rows, explained mismatches, note): printed by conftest's terminal summary
+
+
+def log_parity(label, rows, explained, note=""):
+    PARITY_LOG.append((label, int(rows), int(explained), note))
+
+
+class Widen:
+    """Row accessor over stored logits (fp32, or bf16 bit patterns as uint16):
+    x[b, c] -> that row widened to float64 (what the oracle consumes)."""
+
+    def __init__(self, x, storage):
+        self.x, self.storage = x, storage
+
+    def __getitem__(self, idx):
+        v = self.x[idx]
+        if self.storage == "bf16":
+            return (np.asarray(v).astype(np.uint32) << 16).view(np.float32).astype(np.float64)
+        return np.asarray(v, dtype=np.float64)
+
+
+def oracle_threaded(oracle, kind, zp, zq, ids, u, storage="f32", alpha=-1e3, beta=1e3, chunk=4, threads=None):
+    """The oracle over all batch rows, row chunks in parallel threads (rows are
+    independent, verify_reference.cpp:87-109; the ctypes calls release the
+    GIL).  zp / zq are the STORED logits (widened per chunk, so a C4-sized
+    batch never exists in double at once)."""
+    import os
+    from concurrent.futures import ThreadPoolExecutor
+
+    from oracle.oracle import Result
+
+    B, gamma = ids.shape
+    W = (Widen(zp, storage), Widen(zq, storage))
+
+    def run(lo):
+        hi = min(B, lo + chunk)
+        a, b = W[0][lo:hi], W[1][lo:hi]
+        if kind == "exact":
+            return lo, oracle.verify_exact(a, b, ids[lo:hi], u[lo:hi])
+        return lo, oracle.verify_sigmoid(a, b, ids[lo:hi], u[lo:hi], alpha, beta)
+
+    res = Result(B, gamma)
+    with ThreadPoolExecutor(threads or os.cpu_count() or 1) as ex:
+        for lo, r in ex.map(run, range(0, B, chunk)):
+            hi = lo + len(r.accepted_len)
+            for f in ("accepted_len", "final_token", "resample_used", "tau", "residual_denom"):
+                getattr(res, f)[lo:hi] = getattr(r, f)
+    return res

@@ -9,7 +9,7 @@ import os
 import numpy as np
 import pytest
 
-from tests.parity import compare, round_for, to_device
+from tests.parity import compare, log_parity, round_for, to_device
 
 pytestmark = pytest.mark.gpu
 GOLDEN = os.path.join(os.path.dirname(__file__), "golden", "golden_v1.json")
@@ -56,6 +56,7 @@ def test_golden_vectors(verifier, oracle):
         for k, v in case["expect"].items():
             setattr(exp, k, np.array(v, dtype=getattr(exp, k).dtype))
         mism += compare(exp, r, zp, zq, ids, u, kind, a, b, label=case["id"])
+    log_parity(f"golden vectors (reference outputs, {len(g['cases'])} cases)", len(g["cases"]), mism)
     assert mism <= 1
 
 
@@ -76,6 +77,7 @@ def test_exact_grid(verifier, oracle, dtype):
         o = oracle.verify_exact(zp, zq, ids, u)
         g = _run(verifier, "exact", *to_device(oracle, zp, zq, ids, u, dtype))
         mism += compare(o, g, zp, zq, ids, u, "exact", label=f"grid{i}")
+    log_parity(f"validate-style exact grid {dtype} (40 instances)", 40, mism)
     assert mism <= 1
 
 
@@ -89,6 +91,7 @@ def test_exact_bench_shapes(verifier, oracle, dtype):
         o = oracle.verify_exact(zp, zq, ids, u)
         g = _run(verifier, "exact", *to_device(oracle, zp, zq, ids, u, dtype))
         mism += compare(o, g, zp, zq, ids, u, "exact", label=f"bench{seed}-{B}-{V}")
+    log_parity(f"bench recipe C1 x16 seeds + C2 + C3 {dtype}", 16 + 8 + 64, mism)
     assert mism <= 1
 
 
@@ -108,6 +111,7 @@ def test_sigmoid_grid(verifier, oracle, scale, mag):
         o = oracle.verify_sigmoid(zp, zq, ids, u, -mag, mag)
         g = _run(verifier, "sigmoid", *to_device(oracle, zp, zq, ids, u, "f32"), -mag, mag)
         mism += compare(o, g, zp, zq, ids, u, "sigmoid", -mag, mag, label=f"sig{i}")
+    log_parity(f"validate-style sigmoid grid scale {scale:g} bounds +-{mag:g} (25 instances)", 25, mism)
     assert mism <= 1
 
 
@@ -373,6 +377,7 @@ def test_both_kernels_small_shapes(verifier, oracle, path):
             o = oracle.verify_sigmoid(zp, zq, ids, u, -1e3, 1e3)
             g = _run(verifier, "sigmoid", *to_device(oracle, zp, zq, ids, u, "f32"))
             mism += compare(o, g, zp, zq, ids, u, "sigmoid", label=f"{path}-sig{i}")
+        log_parity(f"small-shape grid forced {path} (24 exact + 24 sigmoid)", 48, mism)
         assert mism <= 1
     finally:
         verifier.set_path("auto")
@@ -424,7 +429,9 @@ def test_c5_sweep_points(verifier, oracle, gamma, B, V, dtype):
         o = _oracle(oracle, kind, zp, zq, ids, u)
         sub = VerifyResult(r.accepted_len[rows], r.final_token[rows], r.resample_used[rows], r.tau[rows],
                            r.residual_denom[rows])
-        assert compare(o, sub, zp, zq, ids, u, kind, label=f"sweep-{kind}-{gamma}-{B}-{V}-{dtype}") <= 1
+        m = compare(o, sub, zp, zq, ids, u, kind, label=f"sweep-{kind}-{gamma}-{B}-{V}-{dtype}")
+        log_parity(f"C5 point g={gamma} B={B} V={V} {dtype} {kind} (row subsample)", len(rows), m)
+        assert m <= 1
 
 
 @pytest.mark.parametrize("mag", [1e3, 1e4, 1e5])
@@ -455,6 +462,7 @@ def test_sigmoid_emulate_half(verifier, oracle, ref, mag):
         same = gn.final_token == o.final_token
         mism += int((~same).sum())
         assert np.all(np.abs(gn.residual_denom - o.residual_denom) <= 1e-6 * np.maximum(1, np.abs(o.residual_denom)))
+    log_parity(f"sigmoid emulate_half vs compiled reference +-{mag:g} (16 instances)", 16, mism)
     assert mism <= 1
 
 
