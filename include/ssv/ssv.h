@@ -105,16 +105,18 @@ int ssv_last_launch_count(const ssv_ctx* ctx);
 #define SSV_PLAN_STREAMING 0
 #define SSV_PLAN_CLUSTER_RESIDENT 1
 #define SSV_PLAN_CLUSTER_RING 2
+#define SSV_PLAN_SLAB 3
 int ssv_last_plan(const ssv_ctx* ctx, int32_t* info, int32_t n);
 
 /* Kernel selection for the verify entry points: AUTO
  * picks the cluster kernel when every batch row can get a resident thread-
- * block cluster, else the streaming kernel.  Both give identical results up to
+ * block cluster, else the streaming kernel.  All give identical results up to
  * the summation order of the fp32 partial sums (same parity bar). */
 #define SSV_PATH_AUTO 0
 #define SSV_PATH_STREAMING 1
 #define SSV_PATH_CLUSTER 2 /* falls back to streaming where the cluster kernel cannot run */
 #define SSV_PATH_CLUSTER_RING 3 /* cluster kernel, two-CTAs-per-SM ring plan only (no resident plan) */
+#define SSV_PATH_SLAB 4 /* exact variant: the slab kernel (experimental; falls back to streaming where it cannot run) */
 int ssv_set_path(ssv_ctx* ctx, int32_t path);
 const char* ssv_version(void);
 

@@ -25,8 +25,9 @@ struct ssv_ctx {
     // stream-ordered scratch
     void* scratch = nullptr;
     size_t scratch_bytes = 0;
-    unsigned* counters = nullptr;  // [2 + 3 * counters_n]: next, exit, cnt1[n], cnt2[n], flag[n] (kernels leave them 0)
-    size_t counters_n = 0;
+    unsigned* counters = nullptr;  // [2]: next, exit (kernels leave them 0)
+    void* slots = nullptr;  // streaming kernel's self-flagging slots (part, gpart): all kSlotEmpty between launches
+    size_t slots_bytes = 0;
     uint32_t* status_dev = nullptr;  // default status word
     // host-entry staging
     void* stage = nullptr;
@@ -116,9 +117,9 @@ int check_shape(ssv_ctx* ctx, int variant, const ssv_verify_args* a, const ssv_v
 }
 
 // Grow the stream-ordered scratch; counters start at zero and the kernels
-// leave them at zero.
-int ensure_scratch(ssv_ctx* ctx, size_t bytes, size_t counters_n) {
-    if (bytes <= ctx->scratch_bytes && counters_n <= ctx->counters_n) return SSV_OK;
+// leave them at zero; slots start empty and the kernels leave them empty.
+int ensure_scratch(ssv_ctx* ctx, size_t bytes, size_t slot_bytes) {
+    if (bytes <= ctx->scratch_bytes && ctx->counters && slot_bytes <= ctx->slots_bytes) return SSV_OK;
     CK(cudaStreamSynchronize(ctx->stream));
     if (bytes > ctx->scratch_bytes) {
         if (ctx->scratch) CK(cudaFree(ctx->scratch));
@@ -127,50 +128,59 @@ int ensure_scratch(ssv_ctx* ctx, size_t bytes, size_t counters_n) {
         CK(cudaMalloc(&ctx->scratch, nb));
         ctx->scratch_bytes = nb;
     }
-    if (counters_n > ctx->counters_n) {
-        if (ctx->counters) CK(cudaFree(ctx->counters));
-        ctx->counters = nullptr;
-        const size_t nn = std::max(counters_n, ctx->counters_n * 2);
-        CK(cudaMalloc(&ctx->counters, (2 + 3 * nn) * sizeof(unsigned)));
+    if (!ctx->counters) {
+        CK(cudaMalloc(&ctx->counters, 2 * sizeof(unsigned)));
         // on the context's stream: the kernels that read the counters follow it
-        CK(cudaMemsetAsync(ctx->counters, 0, (2 + 3 * nn) * sizeof(unsigned), ctx->stream));
-        ctx->counters_n = nn;
+        CK(cudaMemsetAsync(ctx->counters, 0, 2 * sizeof(unsigned), ctx->stream));
+    }
+    if (slot_bytes > ctx->slots_bytes) {
+        if (ctx->slots) CK(cudaFree(ctx->slots));
+        ctx->slots = nullptr;
+        const size_t nb = align_up(std::max(slot_bytes, ctx->slots_bytes * 2));
+        CK(cudaMalloc(&ctx->slots, nb));
+        launch_fill_slots(ctx->slots, nb / sizeof(unsigned long long), ctx->stream);
+        CK(cudaGetLastError());
+        ctx->slots_bytes = nb;
     }
     return SSV_OK;
 }
 
 struct Layout {
-    size_t part, rowstat, dec, gpart, extra, total;
+    size_t rowstat, cgpart, extra, total;  // scratch
+    size_t part, gpart, dslot, slots;      // slot region
 };
 
 Layout plan_scratch(const StepParams& P, size_t extra_bytes) {
     Layout L;
     size_t off = 0;
-    L.part = off;
-    off = align_up(off + (size_t)P.B * std::max(P.NR, 1) * std::max(P.K, 1) * kWarpsPerCta * sizeof(double2));
     L.rowstat = off;
     off = align_up(off + (size_t)P.B * std::max(P.NR, 1) * sizeof(double2));
-    L.dec = off;
-    off = align_up(off + (size_t)P.B * sizeof(Decision));
-    L.gpart = off;
+    L.cgpart = off;
     off = align_up(off + (size_t)P.B * P.NG * sizeof(double2));
     L.extra = off;
     off = align_up(off + extra_bytes);
     L.total = off;
+    off = 0;
+    L.part = off;
+    off = align_up(off + (size_t)P.B * std::max(P.NR, 1) * std::max(P.KP, 1) * sizeof(double2));
+    L.gpart = off;
+    off = align_up(off + (size_t)P.B * P.NG * sizeof(double2));
+    L.dslot = off;
+    off = align_up(off + (size_t)P.B * 3 * sizeof(double2));
+    L.slots = off;
     return L;
 }
 
 void bind_scratch(ssv_ctx* ctx, StepParams& P, const Layout& L) {
     char* s = static_cast<char*>(ctx->scratch);
-    P.part = reinterpret_cast<double2*>(s + L.part);
+    char* z = static_cast<char*>(ctx->slots);
+    P.part = reinterpret_cast<double2*>(z + L.part);
+    P.gpart = reinterpret_cast<double2*>(z + L.gpart);
     P.rowstat = reinterpret_cast<double2*>(s + L.rowstat);
-    P.dec = reinterpret_cast<Decision*>(s + L.dec);
-    P.gpart = reinterpret_cast<double2*>(s + L.gpart);
+    P.dslot = reinterpret_cast<double2*>(z + L.dslot);
+    P.cgpart = reinterpret_cast<double2*>(s + L.cgpart);
     P.next = ctx->counters;
     P.exit_cnt = ctx->counters + 1;
-    P.cnt1 = ctx->counters + 2;
-    P.cnt2 = P.cnt1 + ctx->counters_n;
-    P.flag = P.cnt2 + ctx->counters_n;
 }
 
 int run_device(ssv_ctx* ctx, int variant, const ssv_verify_args* a, ssv_verify_out* o) {
@@ -194,9 +204,14 @@ int run_device(ssv_ctx* ctx, int variant, const ssv_verify_args* a, ssv_verify_o
     P.emulate_half = variant == V_SIGMOID && (a->flags & SSV_EMULATE_HALF) ? 1 : 0;
     const int act = P.emulate_half ? ACT_SIGMOID_HALF : variant;  // the emulation has its own kernels
     plan_geometry(a->dtype, act, P);
-    if (ctx->path != SSV_PATH_STREAMING) plan_cluster(a->dtype, act, P, ctx->path != SSV_PATH_CLUSTER_RING);
+    const bool mat = a->flags & (SSV_WANT_P | SSV_WANT_Q | SSV_WANT_RESIDUAL);
+    if (ctx->path != SSV_PATH_STREAMING && ctx->path != SSV_PATH_SLAB)
+        plan_cluster(a->dtype, act, P, ctx->path != SSV_PATH_CLUSTER_RING);
+    // The slab kernel is selected only on request (measured slower than the
+    // streaming kernel on every shape so far).
+    if (P.cl_size == 0 && !mat && ctx->path == SSV_PATH_SLAB) plan_slab(a->dtype, act, P);
     const Layout L = plan_scratch(P, 0);
-    rc = ensure_scratch(ctx, L.total, (size_t)P.B);
+    rc = ensure_scratch(ctx, L.total, L.slots);
     if (rc) return rc;
     bind_scratch(ctx, P, L);
     P.acc = o->accepted_len;
@@ -210,7 +225,7 @@ int run_device(ssv_ctx* ctx, int variant, const ssv_verify_args* a, ssv_verify_o
     ctx->launches = 0;
     // kernel, cluster size, threads, slots, rows, pieces (ssv_last_plan)
     ctx->plan[0] = P.cl_size > 0 ? (P.cl_resident ? SSV_PLAN_CLUSTER_RESIDENT : SSV_PLAN_CLUSTER_RING)
-                                 : SSV_PLAN_STREAMING;
+                                 : (P.sl_on ? SSV_PLAN_SLAB : SSV_PLAN_STREAMING);
     ctx->plan[1] = P.cl_size;
     ctx->plan[2] = P.cl_size > 0 ? P.cl_threads : kCtaThreads;
     ctx->plan[3] = P.cl_slots;
@@ -372,7 +387,7 @@ int ssv_create(int device, ssv_ctx** out) {
     if (cudaSetDevice(device) != cudaSuccess ||
         cudaStreamCreateWithFlags(&ctx->own, cudaStreamNonBlocking) != cudaSuccess ||
         cudaMalloc(&ctx->status_dev, sizeof(uint32_t)) != cudaSuccess ||
-        cudaMemset(ctx->status_dev, 0, sizeof(uint32_t)) != cudaSuccess ||
+        cudaMemsetAsync(ctx->status_dev, 0, sizeof(uint32_t), ctx->own) != cudaSuccess ||
         cudaEventCreateWithFlags(&ctx->handover, cudaEventDisableTiming) != cudaSuccess ||
         cudaMallocHost(&ctx->status_host, sizeof(uint32_t)) != cudaSuccess) {
         ssv_destroy(ctx);
@@ -398,6 +413,7 @@ void ssv_destroy(ssv_ctx* ctx) {
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
     if (ctx->scratch) cudaFree(ctx->scratch);
     if (ctx->counters) cudaFree(ctx->counters);
+    if (ctx->slots) cudaFree(ctx->slots);
     if (ctx->status_dev) cudaFree(ctx->status_dev);
     if (ctx->stage) cudaFree(ctx->stage);
     if (ctx->hstage) cudaFreeHost(ctx->hstage);
@@ -443,7 +459,8 @@ int ssv_last_plan(const ssv_ctx* ctx, int32_t* info, int32_t n) {
 
 int ssv_set_path(ssv_ctx* ctx, int32_t path) {
     if (!ctx) return SSV_EINVAL;
-    if (path != SSV_PATH_AUTO && path != SSV_PATH_STREAMING && path != SSV_PATH_CLUSTER && path != SSV_PATH_CLUSTER_RING)
+    if (path != SSV_PATH_AUTO && path != SSV_PATH_STREAMING && path != SSV_PATH_CLUSTER && path != SSV_PATH_CLUSTER_RING &&
+        path != SSV_PATH_SLAB)
         return fail(ctx, SSV_EINVAL, "ssv_set_path: unknown path %d", path);
     ctx->path = path;
     return SSV_OK;
@@ -568,7 +585,7 @@ int ssv_sample_softmax(ssv_ctx* ctx, int32_t dtype, const void* logits, int32_t 
     P.sample_mode = 1;
     plan_geometry(dtype, ACT_SOFTMAX, P);
     const Layout L = plan_scratch(P, 0);
-    int rc = ensure_scratch(ctx, L.total, (size_t)rows);
+    int rc = ensure_scratch(ctx, L.total, L.slots);
     if (rc) return rc;
     bind_scratch(ctx, P, L);
     P.fin = tokens_out;
@@ -597,7 +614,7 @@ int ssv_make_bench_inputs(ssv_ctx* ctx, uint64_t seed, int32_t B, int32_t gamma,
     P.sample_mode = 1;
     plan_geometry(dtype, ACT_SOFTMAX, P);
     const Layout L = plan_scratch(P, (size_t)B * gamma * sizeof(double));
-    int rc = ensure_scratch(ctx, L.total, (size_t)B * gamma);
+    int rc = ensure_scratch(ctx, L.total, L.slots);
     if (rc) return rc;
     double* draft_u = reinterpret_cast<double*>(static_cast<char*>(ctx->scratch) + L.extra);
     int launches = 0;

@@ -40,6 +40,7 @@
 #include "ssv_launch.h"
 #include "ssv_device.cuh"
 #include "ssv_pipe.cuh"
+#include "ssv_exptab.h"
 
 #include <cooperative_groups.h>
 
@@ -63,7 +64,6 @@ struct Shared {
     unsigned item, item_next;
     Decision dec;
     double2 wpart[kWarps];
-    double2 gpart2[kWarps * kBG];
     double2 rs[kMaxRowsSmem];
     double loc_d[4];  // locate: carry, denominator, bonus-row max / sum
     int loc_g, loc_useA;
@@ -133,6 +133,32 @@ __device__ __forceinline__ double ratio_clamped(double p, double q) {  // dist.c
     return fmin(1.0, p / q);
 }
 
+// Decision of batch row b as three self-flagging slots (StepParams::dslot):
+// (mode, row), (Mp, Sp), (Mq, Sq).  Written once by the decide step, polled
+// by every consumer, cleared by the row's locate once all consumers are done.
+__device__ __forceinline__ void publish_decision(const StepParams& P, int b, const Decision& d) {
+    st_slot(&P.dslot[3 * b + 1], make_double2(d.Mp, d.Sp));
+    st_slot(&P.dslot[3 * b + 2], make_double2(d.Mq, d.Sq));
+    st_slot(&P.dslot[3 * b + 0], make_double2((double)d.mode, (double)d.row));
+}
+__device__ __forceinline__ bool try_decision(const StepParams& P, int b, Decision& d) {
+    double2 a, x, y;
+    const bool ok = ld_slot(&P.dslot[3 * b + 0], a, kSlotEmpty) & ld_slot(&P.dslot[3 * b + 1], x, kSlotEmpty) &
+                    ld_slot(&P.dslot[3 * b + 2], y, kSlotEmpty);
+    d.mode = (int)a.x;
+    d.row = (int)a.y;
+    d.Mp = x.x;
+    d.Sp = x.y;
+    d.Mq = y.x;
+    d.Sq = y.y;
+    return ok;
+}
+__device__ __forceinline__ Decision wait_decision(const StepParams& P, int b) {
+    Decision d;
+    while (!try_decision(P, b, d)) __nanosleep(32);
+    return d;
+}
+
 // ---------------------------------------------------------------------------
 // Item order.  Segment t holds, in order, the A-items of batch row t - off[A],
 // the D-item of t - off[D], the B-items of t - off[B] and the L-item of
@@ -156,14 +182,6 @@ __device__ __forceinline__ ItemRef decode_item(const StepParams& P, unsigned i) 
         o -= P.nph[p];
     }
     return {IT_L, 0, 0};  // unreachable
-}
-
-__device__ __forceinline__ void red_release_add(unsigned* p, unsigned v) {
-    asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-
-__device__ __forceinline__ void wait_geq(const unsigned* p, unsigned v) {
-    while (ld_acquire(p) < v) __nanosleep(40);
 }
 
 // ---------------------------------------------------------------------------
@@ -448,8 +466,7 @@ __device__ void item_A(const StepParams& P, int b, int idx, const ItemRef& nxt, 
     if (lane == 0) {
         if (isnan(S) || M == CUDART_INF) flag(P, SSV_STATUS_NONFINITE);
         if (S == 0.0) M = -CUDART_INF;  // a warp that saw pads only
-        P.part[(((size_t)b * P.NR + r) * P.K + q) * kWarps + warp] = make_double2(M, S);
-        red_release_add(&P.cnt1[b], 1u);  // release: the partial is visible first
+        st_slot(&P.part[(((size_t)b * P.NR + r) * P.K + q) * kWarps + warp], make_double2(M, S));
     }
 }
 
@@ -459,7 +476,60 @@ __device__ void item_A(const StepParams& P, int b, int idx, const ItemRef& nxt, 
 // activation.cpp:20-27 + verify_reference.cpp:87-92), first rejection
 // (verify_reference.cpp:93-96, inclusive u <= tau).  Runs on the CTA that
 // completed the row's last A-item; publishes Decision + release flag.
-template <typename T>
+// e^-n for an integer n >= 0 (table; 0 past fp64 underflow).
+__device__ __forceinline__ double exp_neg_int(double n) {
+    return n < (double)kExpNegN ? __ldg(&kExpNeg[(int)n]) : 0.0;
+}
+
+// Slab partials carry integer references R = ceil(slice max): two rows'
+// slots folded per warp with every load of a chunk in flight, the rescale
+// factors e^(R_s - R) read from kExpNeg (no fp64 exp on the decision path).
+__device__ __forceinline__ void fold_int_ref2(double2* pa, double2* pb, int KP, double2& ra, double2& rb) {
+    constexpr int NPL = 6;  // slots per lane per row per chunk (12 loads in flight)
+    const int lane = threadIdx.x & 31;
+    double m[2] = {-CUDART_INF, -CUDART_INF}, sm[2] = {0.0, 0.0};
+    double2* pr[2] = {pa, pb};
+    for (int k0 = 0; k0 < KP; k0 += NPL * 32) {
+        double2 v[2][NPL];
+        bool ok[2][NPL];
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+#pragma unroll
+            for (int i = 0; i < NPL; ++i) {
+                const int k = k0 + lane + 32 * i;
+                const bool in = pr[h] != nullptr && k < KP;
+                ok[h][i] = in ? ld_slot(&pr[h][k], v[h][i], kSlotEmpty) : true;
+                if (!in) v[h][i] = make_double2(-CUDART_INF, 0.0);
+            }
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            double cm = -CUDART_INF;
+#pragma unroll
+            for (int i = 0; i < NPL; ++i) {
+                if (!ok[h][i]) v[h][i] = ld_slot_wait(&pr[h][k0 + lane + 32 * i], kSlotEmpty);
+                cm = fmax(cm, v[h][i].x);
+            }
+            if (cm > m[h]) {
+                if (sm[h] != 0.0) sm[h] *= exp_neg_int(cm - m[h]);
+                m[h] = cm;
+            }
+#pragma unroll
+            for (int i = 0; i < NPL; ++i)
+                if (v[h][i].y != 0.0) sm[h] += v[h][i].y * exp_neg_int(m[h] - v[h][i].x);  // NaN propagates
+        }
+    }
+    double2 r[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        const double M = warp_max(m[h]);
+        if (sm[h] != 0.0) sm[h] *= exp_neg_int(M - m[h]);
+        r[h] = make_double2(M, warp_sum(sm[h]));
+    }
+    ra = r[0];
+    rb = r[1];
+}
+
+template <typename T, bool SLAB = false>
 __device__ void item_D(const StepParams& P, int b, Shared& sh) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int G = P.G;
@@ -476,31 +546,67 @@ __device__ void item_D(const StepParams& P, int b, Shared& sh) {
         zq = load_exact(q_row<T>(P, b, tid) + x);
     }
     if (tid <= G) u = P.u[(size_t)b * (G + 1) + tid];
-    if (tid == 0) {
-        wait_geq(&P.cnt1[b], (unsigned)P.nA * kWarps);
-        trace(P, 8 * b + 1);
-    }
-    __syncthreads();
-    const int KP = P.K * kWarps;  // partials per statistics row
-    for (int r = warp; r < P.NR; r += kWarps) {
-        const double2* part = P.part + ((size_t)b * P.NR + r) * KP;
-        double2 pk[4];
-        double m = -CUDART_INF;
+    const int KP = P.KP;  // partial slots per statistics row
+    if constexpr (SLAB) {  // slab partials: integer references, two rows per pass
+        for (int r0 = warp; r0 < P.NR; r0 += 2 * kWarps) {
+            const int r1 = r0 + kWarps;
+            double2* pa = P.part + ((size_t)b * P.NR + r0) * KP;
+            double2* pb = r1 < P.NR ? P.part + ((size_t)b * P.NR + r1) * KP : nullptr;
+            double2 st[2];
+            fold_int_ref2(pa, pb, KP, st[0], st[1]);
+            for (int k = lane; k < KP; k += 32) {
+                clear_slot(&pa[k], kSlotEmpty);
+                if (pb) clear_slot(&pb[k], kSlotEmpty);
+            }
+            if (lane == 0) {
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            const int k = lane + 32 * i;
-            pk[i] = k < KP ? __ldcg(&part[k]) : make_double2(-CUDART_INF, 0.0);
-            m = fmax(m, pk[i].x);
+                for (int h = 0; h < 2; ++h) {
+                    const int r = h ? r1 : r0;
+                    if (r >= P.NR) continue;
+                    if (!isfinite(st[h].x) || !isfinite(st[h].y)) flag(P, SSV_STATUS_NONFINITE);  // NaN / +inf logit
+                    P.rowstat[(size_t)b * P.NR + r] = st[h];
+                    if (r < kMaxRowsSmem) sh.rs[r] = st[h];
+                }
+            }
         }
-        for (int k = lane + 128; k < KP; k += 32) m = fmax(m, __ldcg(&part[k].x));
-        m = warp_max(m);
-        double sm = 0.0;
+    }
+    for (int r = SLAB ? P.NR : warp; r < P.NR; r += kWarps) {
+        // Each partial slot is its own completion flag (written once by its
+        // A-item, no counter): wait for the row's slots, fold, and leave
+        // them empty for the next launch.
+        double2* part = P.part + ((size_t)b * P.NR + r) * KP;
+        // Chunks of 8 slots per lane with every load in flight (the slab
+        // path folds ~300 slots per row), merged into a per-lane running
+        // (max, sum) in fp64, then the warp fold.
+        double m = -CUDART_INF, sm = 0.0;
+        for (int k0 = 0; k0 < KP; k0 += 8 * 32) {
+            double2 v[8];
+            bool ok[8];
 #pragma unroll
-        for (int i = 0; i < 4; ++i)
-            if (pk[i].y != 0.0) sm += pk[i].y * exp(pk[i].x - m);  // NaN propagates
-        for (int k = lane + 128; k < KP; k += 32) {
-            const double2 v = __ldcg(&part[k]);
-            if (v.y != 0.0) sm += v.y * exp(v.x - m);
+            for (int i = 0; i < 8; ++i) {
+                const int k = k0 + lane + 32 * i;
+                ok[i] = k < KP ? ld_slot(&part[k], v[i], kSlotEmpty) : true;
+                if (k >= KP) v[i] = make_double2(-CUDART_INF, 0.0);
+            }
+            double cm = -CUDART_INF;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                if (!ok[i]) v[i] = ld_slot_wait(&part[k0 + lane + 32 * i], kSlotEmpty);
+                cm = fmax(cm, v[i].x);
+            }
+            if (cm > m) {
+                if (sm != 0.0) sm *= exp(m - cm);
+                m = cm;
+            }
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+                if (v[i].y != 0.0) sm += v[i].y * exp(v[i].x - m);  // NaN propagates
+        }
+        for (int k = lane; k < KP; k += 32) clear_slot(&part[k], kSlotEmpty);
+        {
+            const double M = warp_max(m);
+            sm = sm != 0.0 ? sm * exp(m - M) : sm;
+            m = M;
         }
         sm = warp_sum(sm);
         if (lane == 0) {
@@ -510,6 +616,7 @@ __device__ void item_D(const StepParams& P, int b, Shared& sh) {
         }
     }
     __syncthreads();
+    if (tid == 0) trace(P, 8 * b + 1);
     auto rs = [&](int r) -> double2 { return r < kMaxRowsSmem ? sh.rs[r] : __ldcg(&P.rowstat[(size_t)b * P.NR + r]); };
     auto tau_at = [&](int c, double zpc, double zqc) -> double {
         const double2 sp = rs(c), sq = rs(G + c);
@@ -561,9 +668,7 @@ __device__ void item_D(const StepParams& P, int b, Shared& sh) {
             P.rsu[b] = 0;
             P.rden[b] = 0.0;
         }
-        P.dec[b] = d;
-        P.cnt1[b] = 0;  // every A-item of b has been counted
-        st_release(&P.flag[b], 1u);
+        publish_decision(P, b, d);
     }
 }
 
@@ -925,9 +1030,7 @@ __device__ void locate(const StepParams& P, int b, const Decision& d, Shared& sh
     const T* qr = d.mode == MODE_REJECT ? q_row<T>(P, b, d.row) : nullptr;
     // u = u_final (verify_reference.cpp:98), loaded by the caller ahead of time
     if (P.trace && b == 0 && threadIdx.x == 0) trace(P, 8 * P.B + 21);
-    const int ncache = min(NG, kLocCap);
-    for (int g = threadIdx.x; g < ncache; g += NT) gcache[g] = __ldcg(&gp[g]);
-    __syncthreads();
+    // (the caller has cached granules [0, kLocCap) in gcache)
     const long long cyc0 = clock64();
     auto raw = [&](int g) -> double2 { return g < kLocCap ? gcache[g] : __ldcg(&gp[g]); };
 
@@ -1069,18 +1172,7 @@ __device__ void get_decision(const StepParams& P, int b, bool write, Shared& sh)
             sh.dec = d;
         }
     } else {
-        if (tid == 0) {
-            while (ld_acquire(&P.flag[b]) == 0u) __nanosleep(40);
-            const Decision* dp = &P.dec[b];
-            Decision d;
-            d.mode = __ldcg(&dp->mode);
-            d.row = __ldcg(&dp->row);
-            d.Mp = __ldcg(&dp->Mp);
-            d.Sp = __ldcg(&dp->Sp);
-            d.Mq = __ldcg(&dp->Mq);
-            d.Sq = __ldcg(&dp->Sq);
-            sh.dec = d;
-        }
+        if (tid == 0) sh.dec = wait_decision(P, b);
     }
     (void)write;
     __syncthreads();
@@ -1095,8 +1187,7 @@ __device__ void item_D_gather(const StepParams& P, int b, Shared& sh) {
     decide_gather<T, ACT>(P, b, true, sh.dec);
     __syncwarp();
     if (threadIdx.x == 0) {
-        P.dec[b] = sh.dec;
-        st_release(&P.flag[b], 1u);
+        publish_decision(P, b, sh.dec);
         trace(P, 8 * b + 2);
     }
 }
@@ -1122,6 +1213,10 @@ __device__ void item_B(const StepParams& P, int b, int j, Shared& sh) {
     get_decision<T, ACT>(P, b, false, sh);
     if (j == 0 && tid == 0) trace(P, 8 * b + 4);
     const Decision d = sh.dec;
+    // Each warp stores its granule partials straight into their slots (the
+    // value is the completion flag; with no row left to sample the slots
+    // still carry zeros, so the L-item knows every B-item has read the flag).
+    double2* out = P.gpart + (size_t)b * P.NG;
     if (d.mode != MODE_NONE) {
         GranuleData<T> D[kBG];
 #pragma unroll
@@ -1129,16 +1224,15 @@ __device__ void item_B(const StepParams& P, int b, int j, Shared& sh) {
 #pragma unroll
         for (int k = 0; k < kBG; ++k) {
             const double2 gp = granule_reduce<T, ACT>(P, d, D[k]);
-            if (lane == 0) sh.gpart2[k * kWarps + warp] = gp;
+            const int g = g0 + k * kWarps + warp;
+            if (lane == 0 && g < P.NG) st_slot(&out[g], gp);
         }
-        __syncthreads();
-    }
-    if (tid == 0) {
-        if (d.mode != MODE_NONE) {
-            double2* out = P.gpart + (size_t)b * P.NG;
-            for (int w = 0; w < kWarps * kBG && g0 + w < P.NG; ++w) out[g0 + w] = sh.gpart2[w];
+    } else if (lane == 0) {
+#pragma unroll
+        for (int k = 0; k < kBG; ++k) {
+            const int g = g0 + k * kWarps + warp;
+            if (g < P.NG) st_slot(&out[g], make_double2(0.0, 0.0));
         }
-        red_release_add(&P.cnt2[b], 1u);
     }
 }
 
@@ -1151,19 +1245,22 @@ __device__ void item_L(const StepParams& P, int b, Shared& sh, double2* gcache) 
     const double u = __ldcg(&P.u[(size_t)b * (P.G + 1) + P.G]);  // u_final, issued before the waits
     get_decision<T, ACT>(P, b, true, sh);
     const Decision d = sh.dec;
-    if (tid == 0) {
-        wait_geq(&P.cnt2[b], (unsigned)P.nB);
-        trace(P, 8 * b + 6);
+    // Wait for every granule slot of b (each B-item fills its own), caching
+    // the first kLocCap for the locate.
+    double2* gp = P.gpart + (size_t)b * P.NG;
+    for (int g = tid; g < P.NG; g += kCtaThreads) {
+        const double2 v = ld_slot_wait(&gp[g], kSlotEmpty);
+        if (g < kLocCap) gcache[g] = v;
     }
     __syncthreads();
+    if (tid == 0) trace(P, 8 * b + 6);
     if (d.mode != MODE_NONE) {
         locate<T, ACT>(P, b, d, sh, gcache, u);
         if (tid == 0) trace(P, 8 * b + 7);
     }
-    if (tid == 0) {  // every B-item of b has read the flag and been counted
-        P.cnt2[b] = 0;
-        P.flag[b] = 0;
-    }
+    __syncthreads();  // the locate has read the slots
+    for (int g = tid; g < P.NG; g += kCtaThreads) clear_slot(&gp[g], kSlotEmpty);
+    if (tid < 3) clear_slot(&P.dslot[3 * b + tid], kSlotEmpty);  // every B-item has read it (its slots are filled)
 }
 
 // ---------------------------------------------------------------------------
@@ -1226,6 +1323,276 @@ __global__ void __launch_bounds__(kCtaThreads, kCtaMinBlocks) k_verify(StepParam
             *P.next = 0;
         }
     }
+}
+
+// ---------------------------------------------------------------------------
+// K1s k_verify_slab<T>: the slab path (exact variant, large batches; DESIGN.md
+// 3.3).  One persistent CTA per SM, units assigned statically: CTA c takes
+// units c, c + grid, c + 2 grid, ...  Unit u = (b, s) is slice s (kSlabVec
+// 16-byte vectors: 512 fp32 / 1024 bf16 elements) of ALL 2*gamma drafted rows
+// of batch row b, copied once into a shared-memory buffer and kept there until
+// b's decision is known, so the rejected pair is never re-read from HBM.
+// Step k of a CTA:
+//   1. cp.async the unit of step k + Dp into its buffer (Dp units in flight);
+//   2. statistics of step k: one warp per row slice -> (max, sum e^(x-max))
+//      into its self-flagging partial slot; the CTA holding the LAST slice of
+//      b then folds b's partials (item_D: fixed order, fp64), computes tau at
+//      every position and the first rejection, and publishes the decision;
+//   3. residual of step k - L (its buffer still resident): granule masses of
+//      the rejected pair (from shared memory) or the bonus row (global), into
+//      granule slots; the CTA that decided b runs b's inverse CDF (locate)
+//      once all of b's granule slots are filled.
+// Every wait is on work of an earlier step, or of the same step's earlier
+// phase (statistics never wait), so with all CTAs co-resident (cooperative
+// launch) the schedule cannot deadlock; L >= ceil((NS - 1) / grid) keeps a
+// residual from waiting on a decision of a later step.
+constexpr int kSlabVec = 128;                 // 16-byte vectors per row slice (2 KB)
+constexpr int kSlabVPR = kSlabVec + 2;        // shared-memory vectors per row slice (aligned superset)
+constexpr int kSlabRowBytes = kSlabVPR * 16;  // 2080 B
+constexpr int kSlabGcache = kLocCap * (int)sizeof(double2);  // locate's granule cache (16 KB)
+
+template <typename T>
+struct SlabSlice {
+    const uint4* a0;  // 16-byte-aligned start of the slice's superset
+    int shift;        // elements of a0's first vector before the slice
+    int len;          // elements in the slice
+    int nvec;         // vectors of the superset
+};
+
+template <typename T>
+__device__ __forceinline__ SlabSlice<T> slab_slice(const StepParams& P, int b, int r, int s) {
+    constexpr int VEC = Elem<T>::VEC;
+    constexpr int SE = kSlabVec * VEC;
+    const T* row = r < P.G ? p_row<T>(P, b, r) : q_row<T>(P, b, r - P.G);
+    const int e0 = s * SE;
+    const uintptr_t g = reinterpret_cast<uintptr_t>(row + e0);
+    SlabSlice<T> x;
+    x.a0 = reinterpret_cast<const uint4*>(g & ~uintptr_t(15));
+    x.shift = (int)((g & 15) / sizeof(T));
+    x.len = min(SE, P.V - e0);
+    x.nvec = (x.shift + x.len + VEC - 1) / VEC;
+    return x;
+}
+
+// cp.async every drafted row slice of unit (b, s) into buffer `buf`: warp w
+// copies rows w, w + 8, ... (slice geometry once per row, then one 16-byte
+// copy per lane and vector).
+template <typename T>
+__device__ __forceinline__ void slab_issue(const StepParams& P, int b, int s, uint8_t* buf) {
+    const int lane = threadIdx.x & 31;
+    for (int r = threadIdx.x >> 5; r < 2 * P.G; r += kWarps) {
+        const SlabSlice<T> x = slab_slice<T>(P, b, r, s);
+        uint8_t* dst = buf + r * kSlabRowBytes;
+#pragma unroll
+        for (int t = 0; t < (kSlabVPR + 31) / 32; ++t) {
+            const int j = lane + 32 * t;
+            if (j < x.nvec) cp_async16(dst + j * 16, x.a0 + j);
+        }
+    }
+}
+
+// One warp: (R, sum e^(x - R)) of row slice x staged at `rowp`, R = ceil of
+// the slice max.  fp32 pair sums of <= 8 terms widened to fp64,
+// fp64 warp fold.
+template <typename T>
+__device__ __forceinline__ double2 slab_row_stats(const StepParams& P, const uint4* rowp, const SlabSlice<T>& x) {
+    constexpr int VEC = Elem<T>::VEC;
+    constexpr int NV = (kSlabVPR + 31) / 32;  // 5 vectors per lane (the 5th only on lanes 0, 1)
+    constexpr int GRP = VEC == 4 ? 4 : 2;     // vectors per fp32 group: 8 terms per pair lane
+    const int lane = threadIdx.x & 31;
+    uint4 w[NV];
+    float m = -FLT_MAX, mn = FLT_MAX;
+#pragma unroll
+    for (int t = 0; t < NV; ++t) {
+        const int j = lane + 32 * t;
+        w[t] = j < x.nvec ? rowp[j] : pad_vec<T>();
+    }
+    if (x.shift != 0 || x.len != kSlabVec * VEC) {  // misaligned or short slice: pad the edge vectors (warp-uniform)
+#pragma unroll
+        for (int t = 0; t < NV; ++t) {
+            const int j = lane + 32 * t;
+            if (j < x.nvec && (j == 0 || j == x.nvec - 1))
+                mask_vec<T>(w[t], max(0, x.shift - j * VEC), min(VEC, x.shift + x.len - j * VEC));
+        }
+    }
+#pragma unroll
+    for (int t = 0; t < NV; ++t) AStat<T>::minmax(w[t], m, mn);
+    m = ceilf(warp_max(m));  // integer reference >= the slice max (fold: e^(R_s - R) from kExpNeg)
+    double S = 0.0;
+    const float2 negM = make_float2(-m, -m);
+#pragma unroll
+    for (int t0 = 0; t0 < NV; t0 += GRP) {
+        float2 a = make_float2(0.f, 0.f);
+#pragma unroll
+        for (int t = t0; t < t0 + GRP && t < NV; ++t) AStat<T>::expsum(w[t], negM, a);
+        S += (double)a.x + (double)a.y;
+    }
+    S = warp_sum(S);
+    if (__any_sync(kFull, !isfinite(mn)) && lane == 0) flag(P, SSV_STATUS_NONFINITE);  // -inf / NaN logit
+    return make_double2((double)m, S);
+}
+
+// Raw loads of b's decision slots, issued a step before they are needed (the
+// words are decoded -- and the load latency paid -- only at the next step).
+struct DecRaw {
+    unsigned long long w[6];
+};
+__device__ __forceinline__ void dec_issue(const StepParams& P, int b, DecRaw& r) {
+    const double2* p = P.dslot + 3 * b;
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+        asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(r.w[2 * i]), "=l"(r.w[2 * i + 1]) : "l"(p + i)
+                     : "memory");
+}
+__device__ __forceinline__ bool dec_decode(const DecRaw& r, Decision& d) {
+    bool ok = true;
+#pragma unroll
+    for (int i = 0; i < 6; ++i) ok &= r.w[i] != kSlotEmpty;
+    d.mode = (int)__longlong_as_double((long long)r.w[0]);
+    d.row = (int)__longlong_as_double((long long)r.w[1]);
+    d.Mp = __longlong_as_double((long long)r.w[2]);
+    d.Sp = __longlong_as_double((long long)r.w[3]);
+    d.Mq = __longlong_as_double((long long)r.w[4]);
+    d.Sq = __longlong_as_double((long long)r.w[5]);
+    return ok;
+}
+
+// Inverse CDF of batch row b once all of its granule slots are filled; then
+// b's granule and decision slots are left empty for the next launch.
+template <typename T>
+__device__ void slab_locate(const StepParams& P, int b, Shared& sh, double2* gcache) {
+    const int tid = threadIdx.x, G = P.G;
+    const double uf = __ldcg(&P.u[(size_t)b * (G + 1) + G]);
+    if (tid == 0) sh.dec = wait_decision(P, b);
+    double2* gp = P.gpart + (size_t)b * P.NG;
+    for (int g0 = 0; g0 < P.NG; g0 += 4 * kCtaThreads) {  // four slots per thread in flight
+        double2 v[4];
+        bool ok[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int g = g0 + tid + i * kCtaThreads;
+            ok[i] = g < P.NG ? ld_slot(&gp[g], v[i], kSlotEmpty) : true;
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int g = g0 + tid + i * kCtaThreads;
+            if (!ok[i]) v[i] = ld_slot_wait(&gp[g], kSlotEmpty);
+            if (g < P.NG && g < kLocCap) gcache[g] = v[i];
+        }
+    }
+    __syncthreads();
+    const Decision d = sh.dec;
+    if (tid == 0) trace(P, 8 * b + 6);
+    if (d.mode != MODE_NONE) locate<T, ACT_SOFTMAX>(P, b, d, sh, gcache, uf);
+    if (tid == 0) trace(P, 8 * b + 7);
+    __syncthreads();
+    for (int g = tid; g < P.NG; g += kCtaThreads) clear_slot(&gp[g], kSlotEmpty);
+    if (tid < 3) clear_slot(&P.dslot[3 * b + tid], kSlotEmpty);
+    __syncthreads();
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kCtaThreads, 1) k_verify_slab(StepParams P) {
+    __shared__ Shared sh;
+    extern __shared__ __align__(128) uint8_t slab_smem[];
+    constexpr int VEC = Elem<T>::VEC;
+    constexpr int SE = kSlabVec * VEC;
+    constexpr int GPSL = SE / kGW;  // granules per slice (1 fp32, 2 bf16)
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int G = P.G, NRd = 2 * G, NS = P.sl_ns, nbuf = P.sl_nbuf, Dp = P.sl_dp, L = P.sl_lag;
+    double2* gcache = reinterpret_cast<double2*>(slab_smem + (size_t)nbuf * P.sl_ub);
+    pdl_enter();
+    const int NU = P.B * NS;
+    const int grid = gridDim.x, c = blockIdx.x;
+    const int nsteps = c < NU ? (NU - c + grid - 1) / grid : 0;
+    auto bufp = [&](int slot) { return slab_smem + (size_t)slot * P.sl_ub; };
+    if (P.trace && c == 0 && tid == 0) trace(P, 8 * P.B);
+    // Unit of step k: u = c + k * grid = (b, s); tracked incrementally.
+    auto unit_bs = [&](int k, int& b, int& s) {
+        const int u = c + k * grid;
+        b = u / NS;
+        s = u - b * NS;
+    };
+    for (int k = 0; k < Dp; ++k) {
+        if (k < nsteps) {
+            int b, s;
+            unit_bs(k, b, s);
+            slab_issue<T>(P, b, s, bufp(k % nbuf));
+        }
+        cp_async_commit();
+    }
+    DecRaw pre;  // thread 0: the next residual step's decision words, in flight (issued at step k - 1)
+    int slot_k = 0;                         // buffer of step k
+    int slot_i = Dp % nbuf;                 // buffer of step k + Dp
+    int slot_r = (nbuf - L % nbuf) % nbuf;  // buffer of step k - L
+    for (int k = 0; k < nsteps + L; ++k) {
+        if (k + Dp < nsteps) {
+            int b, s;
+            unit_bs(k + Dp, b, s);
+            slab_issue<T>(P, b, s, bufp(slot_i));
+        }
+        cp_async_commit();  // (possibly empty: one group per step keeps the wait count fixed)
+        if (k < nsteps) {
+            int b, s;
+            unit_bs(k, b, s);
+            cp_async_wait_pending((unsigned)Dp);
+            __syncthreads();  // unit k has landed (every thread's copies)
+            const uint8_t* buf = bufp(slot_k);
+            for (int r = warp; r < NRd && !(P.dbg & 2); r += kWarps) {
+                const SlabSlice<T> x = slab_slice<T>(P, b, r, s);
+                const double2 st = slab_row_stats<T>(P, reinterpret_cast<const uint4*>(buf + r * kSlabRowBytes), x);
+                if (lane == 0) st_slot(&P.part[((size_t)b * NRd + r) * NS + s], st);
+            }
+            if (s == 0 && tid == 0) trace(P, 8 * b + 3);
+            if (P.trace && tid == 0 && k < 6 && P.sl_dbg) P.trace[8 * P.B + 26 + c * 8 + k] = gtime();
+            if (s == NS - 1 && !(P.dbg & 1)) {  // this CTA decides b (item_D waits for b's other partial slots)
+                if (tid == 0) trace(P, 8 * b);
+                item_D<T, true>(P, b, sh);
+                if (tid == 0) trace(P, 8 * b + 2);
+            }
+        }
+        if (k >= L && !(P.dbg & 1)) {
+            const int kr = k - L;
+            int b, s;
+            unit_bs(kr, b, s);
+            if (tid == 0) {
+                Decision d;
+                if (!dec_decode(pre, d)) d = wait_decision(P, b);
+                sh.dec = d;
+                if (s == 0) trace(P, 8 * b + 4);
+            }
+            __syncthreads();
+            const Decision d = sh.dec;
+            const uint8_t* buf = bufp(slot_r);
+            const int e0 = s * SE;
+            const int ng = min(GPSL, (P.V - e0 + kGW - 1) / kGW);
+            if (warp < ng) {
+                const int g = s * GPSL + warp;
+                double2 out = make_double2(0.0, 0.0);
+                if (d.mode == MODE_REJECT) {
+                    const SlabSlice<T> xp = slab_slice<T>(P, b, d.row, s), xq = slab_slice<T>(P, b, G + d.row, s);
+                    const T* sp = reinterpret_cast<const T*>(buf + d.row * kSlabRowBytes) + xp.shift + warp * kGW;
+                    const T* sq = reinterpret_cast<const T*>(buf + (G + d.row) * kSlabRowBytes) + xq.shift + warp * kGW;
+                    GranuleData<T> D;
+                    granule_load<T, true>(P, b, g, d, D, sp, sq);
+                    out = granule_reduce<T, ACT_SOFTMAX>(P, d, D);
+                } else if (d.mode == MODE_BONUS) {
+                    granule<T, ACT_SOFTMAX>(P, b, g, d, &out);
+                }
+                if (lane == 0) st_slot(&P.gpart[(size_t)b * P.NG + g], out);
+            }
+            if (s == 0 && tid == 0) trace(P, 8 * b + 5);
+            if (P.trace && tid == 0 && kr < 2 && P.sl_dbg) P.trace[8 * P.B + 26 + c * 8 + 6 + kr] = gtime();
+        }
+        if (tid == 0 && k + 1 >= L && k + 1 - L < nsteps) dec_issue(P, (c + (k + 1 - L) * grid) / NS, pre);
+        __syncthreads();  // buffer of step k - L is free; shared state dead
+        slot_k = slot_k + 1 == nbuf ? 0 : slot_k + 1;
+        slot_i = slot_i + 1 == nbuf ? 0 : slot_i + 1;
+        slot_r = slot_r + 1 == nbuf ? 0 : slot_r + 1;
+    }
+    // Inverse CDFs, spread over the CTAs once every residual is in.
+    for (int b = c; b < P.B && !(P.dbg & 1); b += grid) slab_locate<T>(P, b, sh, gcache);
+    if (P.trace && tid == 0) atomicMax(&P.trace[8 * P.B + 1], gtime());
 }
 
 // ---------------------------------------------------------------------------
@@ -1606,7 +1973,7 @@ __global__ void __launch_bounds__(NT, 1) k_verify_cluster(StepParams P) {
             }
             if (lane == 0) {
                 gloc[j] = out;
-                if (g < P.NG) P.gpart[(size_t)b * P.NG + g] = out;
+                if (g < P.NG) P.cgpart[(size_t)b * P.NG + g] = out;
             }
         }
         __syncthreads();
@@ -1747,7 +2114,7 @@ __global__ void __launch_bounds__(NT, 1) k_verify_cluster(StepParams P) {
     }
     __syncthreads();
     if (tl) trace(P, 8 * P.B + 18);
-    const double2* gp = P.gpart + (size_t)b * P.NG;
+    const double2* gp = P.cgpart + (size_t)b * P.NG;
     auto gmass = [&](int g) -> double {  // normalized granule mass (fallback path)
         const double2 v = __ldcg(&gp[g]);
         if (R.mode == MODE_REJECT) return (R.useA ? v.x : v.y) / R.denom;
@@ -1957,12 +2324,11 @@ void plan_geometry(int dtype, int act, StepParams& P) {
         P.K = (P.Kc + P.runA - 1) / P.runA;
         P.nA = P.NR * P.K;
     }
+    P.KP = P.K * kWarps;
     P.nph[IT_A] = P.nA;
     P.nph[IT_D] = P.sample_mode ? 0 : 1;  // exact: row statistics + decision; sigmoid / probs: gathers only
     P.nph[IT_B] = P.nB;
     P.nph[IT_L] = 1;
-    static const bool a_only = knob_set("SSV_AONLY");  // experiment builds only: A phase alone (no results)
-    if (a_only && exact) P.nph[IT_D] = P.nph[IT_B] = P.nph[IT_L] = 0;
     // Phase offsets, in segments of one batch row each: a phase of row b is
     // dispatched about one resident wave after the phase it waits on, so the
     // wait is short and the rejected pair (read by the A-items a few rows
@@ -2279,6 +2645,81 @@ static void launch_cluster_t(const StepParams& P, const Launch& L) {
     L.end(h);
 }
 
+// Slab path geometry (sl_on 0 = not applicable).  One CTA per SM (shared
+// memory sized so), nbuf unit buffers: Dp in flight, one in use, L awaiting
+// their batch row's decision.
+constexpr int kSlabSmemMax = 227 * 1024 - 4096;  // dynamic budget (static Shared + slack)
+
+template <typename T>
+static bool plan_slab_t(StepParams& P) {
+    P.sl_on = 0;
+    if (P.sample_mode || 2 * P.G > kMaxRowsSmem) return false;
+    const int NRd = 2 * P.G;
+    const int ub = NRd * kSlabRowBytes;
+    const int nbuf = std::min((kSlabSmemMax - kSlabGcache) / ub, 16);
+    const int SE = kSlabVec * (int)(16 / sizeof(T));
+    const int NS = (P.V + SE - 1) / SE;
+    const int smem = nbuf * ub + kSlabGcache;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_verify_slab<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSlabSmemMax);
+        attr = true;
+    }
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_verify_slab<T>, kCtaThreads, smem);
+    if (per_sm < 1) return false;
+    const int grid = sm_count() * per_sm;
+    const int Lmin = std::max(1, (NS - 1 + grid - 1) / grid);
+    if (nbuf < Lmin + 2) return false;
+    static const int dp_env = knob("SSV_SLAB_DP", 0);
+    int Dp = dp_env > 0 ? dp_env : (64 * 1024 + ub - 1) / ub;
+    Dp = std::max(1, std::min(Dp, nbuf - 1 - Lmin));
+    P.sl_on = 1;
+    P.sl_ns = NS;
+    P.sl_nbuf = nbuf;
+    P.sl_dp = Dp;
+    P.sl_lag = P.sl_nbuf - 1 - Dp;
+    P.sl_ub = ub;
+    P.sl_smem = P.sl_nbuf * ub + kSlabGcache;
+    P.sl_grid = grid;
+    static const int sl_dbg = knob("SSV_SLAB_TRACE", 0);
+    P.sl_dbg = sl_dbg;
+    static const int dbgm = knob("SSV_DBG_MODE", 0);
+    P.dbg = dbgm;  // experiment bits (slab: 1 statistics only, 2 loads only; results invalid)
+    P.NR = NRd;
+    P.KP = NS;
+    static const bool dbg = knob_set("SSV_DEBUG");
+    if (dbg)
+        fprintf(stderr, "ssv: slab plan B=%d G=%d V=%d NS=%d nbuf=%d Dp=%d L=%d ub=%d smem=%d grid=%d\n", P.B, P.G,
+                P.V, NS, P.sl_nbuf, Dp, P.sl_lag, ub, P.sl_smem, grid);
+    return true;
+}
+
+bool plan_slab(int dtype, int act, StepParams& P) {
+    P.sl_on = 0;
+    if (act != ACT_SOFTMAX) return false;
+    if (dtype == DT_F32) return plan_slab_t<float>(P);
+    if (dtype == DT_BF16) return plan_slab_t<__nv_bfloat16>(P);
+    return false;
+}
+
+template <typename T>
+static void launch_slab_t(const StepParams& P, const Launch& L) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)P.sl_grid, 1, 1);
+    cfg.blockDim = dim3(kCtaThreads, 1, 1);
+    cfg.dynamicSmemBytes = P.sl_smem;
+    cfg.stream = L.st;
+    cudaLaunchAttribute at[2];
+    at[0].id = cudaLaunchAttributeCooperative;  // every CTA co-resident (the schedule's waits need it)
+    at[0].val.cooperative = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1 + pdl_attr(at[1]);
+    const int h = L.begin(KID_VERIFY);
+    cudaLaunchKernelEx(&cfg, k_verify_slab<T>, P);
+    L.end(h);
+}
+
 template <typename T, int ACT>
 static void launch_mat_t(const StepParams& P, void* p, void* q, void* r, const Launch& L) {
     const int h = L.begin(KID_MATERIALIZE);
@@ -2290,6 +2731,9 @@ template <typename T, int ACT>
 static void launch_step_t(const StepParams& P, const Launch& L) {
     if constexpr (sizeof(T) != 8) {
         if (P.cl_size > 0) return launch_cluster_t<T, ACT>(P, L);
+        if constexpr (ACT == ACT_SOFTMAX) {
+            if (P.sl_on) return launch_slab_t<T>(P, L);
+        }
     }
     launch_verify_t<T, ACT>(P, L);
 }
@@ -2332,6 +2776,15 @@ void launch_gen_logits(int dtype, uint64_t seed, int B, int G, int V, void* zp, 
         k_gen_logits<__nv_bfloat16><<<blocks, kThreads, 0, L.st>>>(seed, B, G, V, (__nv_bfloat16*)zp, (__nv_bfloat16*)zq);
     else k_gen_logits<double><<<blocks, kThreads, 0, L.st>>>(seed, B, G, V, (double*)zp, (double*)zq);
     L.end(h);
+}
+
+__global__ void k_fill_slots(unsigned long long* p, size_t n) {
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+        p[i] = kSlotEmpty;
+}
+
+void launch_fill_slots(void* p, size_t n_u64, cudaStream_t st) {
+    k_fill_slots<<<sm_count() * 4, kThreads, 0, st>>>(static_cast<unsigned long long*>(p), n_u64);
 }
 
 void launch_gen_uniforms(uint64_t seed, int B, int G, int V, double* draft_u, double* u, const Launch& L) {

@@ -78,6 +78,11 @@ struct StepParams {
     int cl_threads;  // 256, or 512 for all-resident slices with more rows than 8 warps
     int cl_resident;  // 1: the resident plan (every row slice in shared memory), 0: the ring plan
     int cl_pieces, cl_pe;  // ring units: each row slice in cl_pieces pieces of cl_pe elements
+    // Slab path (exact, large batches, see k_verify_slab): one persistent CTA
+    // per SM; unit u = (b, s) is slice s (kSlabVec 16-byte vectors) of all
+    // 2*gamma drafted rows of batch row b, held in a shared-memory buffer until
+    // b's decision is known.
+    int sl_on, sl_ns, sl_nbuf, sl_dp, sl_lag, sl_ub, sl_smem, sl_grid, sl_dbg;
     int dbg;  // experiment bits (SSV_DBG_MODE), 0 in production
     double alpha, width;
     int sample_mode;     // sample softmax(z_p row b) with u[b] (draft sampling)
@@ -85,15 +90,19 @@ struct StepParams {
     int emulate_half;    // sigmoid: binary16 emulation (SSV_EMULATE_HALF)
     unsigned long long* trace;  // diagnostics: [8*B] per-row phase stamps (tools/trace_step.py), [8*B..+2) kernel start/end
     // scratch
-    double2* part;     // [B][NR][K][8] A-item warp partials (max, sum e^(x-max))
-    double2* rowstat;  // [B][NR]    row (max, sum)
-    Decision* dec;     // [B]
+    // Slots (streaming kernel): each written once per launch with relaxed
+    // stores, polled by its consumer until neither word holds kSlotEmpty, then
+    // reset to kSlotEmpty -- the value is its own completion flag, so the
+    // producers need no release fence (a MEMBAR that would drain their
+    // in-flight cp.async ring).  The slot region is all-empty between launches.
+    double2* part;     // [B][NR][KP] partials (max, sum e^(x-max)): A-item warps / slab slices
     double2* gpart;    // [B][NG]    granule partials
+    double2* dslot;    // [B][3]     decision: (mode, row), (Mp, Sp), (Mq, Sq)
+    int KP;            // partial slots per statistics row
+    double2* rowstat;  // [B][NR]    row (max, sum)
+    double2* cgpart;   // [B][NG]    cluster path: granule partials (last-positive fallback)
     unsigned* next;     // [1] item claim counter   (reset by the last CTA to exit)
     unsigned* exit_cnt; // [1] CTAs done            (reset by the last CTA to exit)
-    unsigned* cnt1;    // [B] A-items done       (reset by the D-item)
-    unsigned* cnt2;    // [B] B-items done       (reset by the L-item)
-    unsigned* flag;    // [B] decision published (reset by the L-item)
     // outputs
     int32_t* acc;
     int32_t* fin;
@@ -134,8 +143,14 @@ struct Launch {
     }
 };
 
+// Empty-slot pattern: a NaN whose low word no computed partial can carry
+// (partials are fp32-derived or fp64 sums: their NaN payloads have zero low bits).
+constexpr unsigned long long kSlotEmpty = 0xFFF0DEADFFF0DEADull;
+
 void plan_geometry(int dtype, int act, StepParams& P);
+void launch_fill_slots(void* p, size_t n_u64, cudaStream_t st);
 bool plan_cluster(int dtype, int act, StepParams& P, bool allow_resident = true);  // small-batch cluster path (sets cl_*)
+bool plan_slab(int dtype, int act, StepParams& P);  // exact, large batches (sets sl_*)
 int trace_slots(const StepParams& P);
 void launch_verify(int dtype, int act, const StepParams& P, void* outp, void* outq, void* outr,
                    const Launch& L);

@@ -79,4 +79,26 @@ __device__ __forceinline__ void st_release(unsigned* p, unsigned v) {
     asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
+// Self-flagging slots (StepParams::part / gpart): a relaxed store of the
+// value; the consumer polls until neither 8-byte word is the empty pattern
+// (each word is single-copy atomic, so a word that is not empty is final).
+__device__ __forceinline__ void st_slot(double2* p, double2 v) {
+    asm volatile("st.relaxed.gpu.global.v2.f64 [%0], {%1, %2};" ::"l"(p), "d"(v.x), "d"(v.y) : "memory");
+}
+__device__ __forceinline__ bool ld_slot(const double2* p, double2& v, unsigned long long empty) {
+    unsigned long long a, b;
+    asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(p) : "memory");
+    v = make_double2(__longlong_as_double((long long)a), __longlong_as_double((long long)b));
+    return a != empty && b != empty;
+}
+__device__ __forceinline__ double2 ld_slot_wait(const double2* p, unsigned long long empty) {
+    double2 v;
+    while (!ld_slot(p, v, empty)) __nanosleep(32);
+    return v;
+}
+__device__ __forceinline__ void clear_slot(double2* p, unsigned long long empty) {
+    const double e = __longlong_as_double((long long)empty);
+    *p = make_double2(e, e);
+}
+
 }  // namespace ssv

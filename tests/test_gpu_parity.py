@@ -355,11 +355,11 @@ def test_full_size_c4_row_subsample(verifier, oracle):
     assert ((r.tau >= 0) & (r.tau <= 1)).all()
 
 
-@pytest.mark.parametrize("path", ["streaming", "cluster", "cluster_ring"])
+@pytest.mark.parametrize("path", ["streaming", "cluster", "cluster_ring", "slab"])
 def test_both_kernels_small_shapes(verifier, oracle, path):
     """The streaming and the cluster kernel each on the small shapes the auto
     choice would route to the other one (validate.cpp:221-321-style grid)."""
-    rng = np.random.default_rng({"streaming": 11, "cluster": 12, "cluster_ring": 13}[path])
+    rng = np.random.default_rng({"streaming": 11, "cluster": 12, "cluster_ring": 13, "slab": 14}[path])
     state = (0x5EED + len(path), 0)
     verifier.set_path(path)
     try:
@@ -391,12 +391,12 @@ def test_streaming_and_cluster_agree_on_c2(verifier, oracle):
     zp, zq = oracle.round_f32(zp), oracle.round_f32(zq)
     t = to_device(oracle, zp, zq, ids, u, "f32")
     res = {}
-    for path in ("streaming", "cluster", "cluster_ring"):
+    for path in ("streaming", "cluster", "cluster_ring", "slab"):
         verifier.set_path(path)
         res[path] = _run(verifier, "exact", *t).numpy()
     verifier.set_path("auto")
     a = res["streaming"]
-    for b in (res["cluster"], res["cluster_ring"]):
+    for b in (res["cluster"], res["cluster_ring"], res["slab"]):
         assert np.array_equal(a.accepted_len, b.accepted_len) and np.array_equal(a.final_token, b.final_token)
         assert np.abs(a.tau - b.tau).max() < 1e-6 and np.abs(a.residual_denom - b.residual_denom).max() < 1e-6
 
@@ -511,7 +511,7 @@ def test_locate_edges(verifier, oracle, path):
         verifier.set_path("auto")
 
 
-@pytest.mark.parametrize("path", ["streaming", "cluster", "cluster_ring"])
+@pytest.mark.parametrize("path", ["streaming", "cluster", "cluster_ring", "slab"])
 def test_locate_edges_exact_logits(verifier, oracle, path):
     """The residual corner cases of test_locate_edges with fp32 LOGITS on the C2
     shape (B=8, gamma=5, V=51865 -- the resident cluster plan, which scans the

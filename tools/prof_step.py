@@ -15,8 +15,10 @@ ap.add_argument("--V", type=int, default=51865)
 ap.add_argument("--dtype", default="f32")
 ap.add_argument("--variant", default="exact")
 ap.add_argument("--iters", type=int, default=4)
+ap.add_argument("--path", default="auto")
 a = ap.parse_args()
 v = Verifier(0)
+v.set_path(a.path)
 dt = {"f32": torch.float32, "bf16": torch.bfloat16}[a.dtype]
 zp, zq, ids, u = v.make_bench_inputs(1, a.B, a.gamma, a.V, dt)
 for _ in range(a.iters):

@@ -15,15 +15,17 @@ ap.add_argument("--gamma", type=int, default=5)
 ap.add_argument("--V", type=int, default=51865)
 ap.add_argument("--dtype", default="f32")
 ap.add_argument("--variant", default="exact")
+ap.add_argument("--path", default="auto")
 a = ap.parse_args()
 v = Verifier(0)
+v.set_path(a.path)
 dt = {"f32": torch.float32, "bf16": torch.bfloat16}[a.dtype]
 zp, zq, ids, u = v.make_bench_inputs(1, a.B, a.gamma, a.V, dt)
 run = (lambda: v.verify_exact(zp, zq, ids, u)) if a.variant == "exact" else (lambda: v.verify_sigmoid(zp, zq, ids, u))
 for _ in range(3):
     run()
 torch.cuda.synchronize()
-cap = 8 * a.B + 26
+cap = 8 * a.B + 26 + 148 * 8
 v.trace_enable(cap)
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 s = torch.cuda.Stream()
@@ -37,6 +39,7 @@ t = v.trace_read(cap).astype(np.int64)
 t0, t1 = t[8 * a.B], t[8 * a.B + 1]
 print(f"event {e0.elapsed_time(e1) * 1e3:.1f} us; kernel span (CTA 0 start -> last CTA end) {(t1 - t0) / 1e3:.1f} us")
 print("streaming: row acc | D claimed stats published | B0 claimed decided | L claimed ready end")
+print("slab:      row acc | D start folded decided | slice0 stats-done residual-decided residual-done | L - start end")
 print("cluster:   row acc | start stats sync1 | decided granules | sync2 gathered locate-end  (us from kernel start)")
 ph = t[: 8 * a.B].reshape(a.B, 8)
 acc = r.accepted_len.cpu().numpy()
@@ -54,3 +57,13 @@ if lo[3] > 0:
     print(f"row-0 locate (us): enter {f2(lo[3])} level1-done {f2(lo[0])} level2-values {f2(lo[1])} end {f2(lo[2])}")
 if t[8 * a.B + 22] > 0:
     print(f"row-0 locate level-1 on warp 0: {int(t[8 * a.B + 22])} cycles")
+
+if os.environ.get("SSV_SLAB_TRACE"):
+    ct = t[8 * a.B + 26: 8 * a.B + 26 + 148 * 8].reshape(148, 8)
+    print("per-CTA: stats-done steps 0..5 | residual-done steps 0..1 (us)")
+    for c in list(range(0, 148, 8)) + [147]:
+        print(f"cta {c:3d} " + " ".join(f(x) for x in ct[c]))
+    for k in range(6):
+        col = ct[:, k][ct[:, k] > 0]
+        if len(col):
+            print(f"step {k}: stats done min {(col.min() - t0) / 1e3:.1f} max {(col.max() - t0) / 1e3:.1f} us")
