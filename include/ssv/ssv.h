@@ -106,6 +106,7 @@ int ssv_last_launch_count(const ssv_ctx* ctx);
 #define SSV_PLAN_CLUSTER_RESIDENT 1
 #define SSV_PLAN_CLUSTER_RING 2
 #define SSV_PLAN_SLAB 3
+#define SSV_PLAN_SIGMOID_STREAM 4
 int ssv_last_plan(const ssv_ctx* ctx, int32_t* info, int32_t n);
 
 /* Kernel selection for the verify entry points: AUTO

@@ -210,6 +210,7 @@ int run_device(ssv_ctx* ctx, int variant, const ssv_verify_args* a, ssv_verify_o
     // The slab kernel is selected only on request (measured slower than the
     // streaming kernel on every shape so far).
     if (P.cl_size == 0 && !mat && ctx->path == SSV_PATH_SLAB) plan_slab(a->dtype, act, P);
+    if (P.cl_size == 0 && ctx->path != SSV_PATH_STREAMING) plan_sig(a->dtype, act, P);
     const Layout L = plan_scratch(P, 0);
     rc = ensure_scratch(ctx, L.total, L.slots);
     if (rc) return rc;
@@ -225,7 +226,7 @@ int run_device(ssv_ctx* ctx, int variant, const ssv_verify_args* a, ssv_verify_o
     ctx->launches = 0;
     // kernel, cluster size, threads, slots, rows, pieces (ssv_last_plan)
     ctx->plan[0] = P.cl_size > 0 ? (P.cl_resident ? SSV_PLAN_CLUSTER_RESIDENT : SSV_PLAN_CLUSTER_RING)
-                                 : (P.sl_on ? SSV_PLAN_SLAB : SSV_PLAN_STREAMING);
+                                 : (P.sl_on ? SSV_PLAN_SLAB : (P.sg_on ? SSV_PLAN_SIGMOID_STREAM : SSV_PLAN_STREAMING));
     ctx->plan[1] = P.cl_size;
     ctx->plan[2] = P.cl_size > 0 ? P.cl_threads : kCtaThreads;
     ctx->plan[3] = P.cl_slots;

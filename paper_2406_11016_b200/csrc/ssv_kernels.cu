@@ -1457,13 +1457,15 @@ __device__ __forceinline__ bool dec_decode(const DecRaw& r, Decision& d) {
     return ok;
 }
 
-// Inverse CDF of batch row b once all of its granule slots are filled; then
-// b's granule and decision slots are left empty for the next launch.
-template <typename T>
-__device__ void slab_locate(const StepParams& P, int b, Shared& sh, double2* gcache) {
+// Inverse CDF of batch row b once all of its granule slots are filled (slab
+// and sigmoid-stream kernels); then b's granule and decision slots are left
+// empty for the next launch.
+template <typename T, int ACT>
+__device__ void locate_row(const StepParams& P, int b, Shared& sh, double2* gcache) {
     const int tid = threadIdx.x, G = P.G;
     const double uf = __ldcg(&P.u[(size_t)b * (G + 1) + G]);
-    if (tid == 0) sh.dec = wait_decision(P, b);
+    DecRaw dr;
+    if (tid == 0) dec_issue(P, b, dr);  // in flight with the granule slots below
     double2* gp = P.gpart + (size_t)b * P.NG;
     for (int g0 = 0; g0 < P.NG; g0 += 4 * kCtaThreads) {  // four slots per thread in flight
         double2 v[4];
@@ -1480,10 +1482,15 @@ __device__ void slab_locate(const StepParams& P, int b, Shared& sh, double2* gca
             if (g < P.NG && g < kLocCap) gcache[g] = v[i];
         }
     }
+    if (tid == 0) {
+        Decision d;
+        if (!dec_decode(dr, d)) d = wait_decision(P, b);
+        sh.dec = d;
+    }
     __syncthreads();
     const Decision d = sh.dec;
     if (tid == 0) trace(P, 8 * b + 6);
-    if (d.mode != MODE_NONE) locate<T, ACT_SOFTMAX>(P, b, d, sh, gcache, uf);
+    if (d.mode != MODE_NONE) locate<T, ACT>(P, b, d, sh, gcache, uf);
     if (tid == 0) trace(P, 8 * b + 7);
     __syncthreads();
     for (int g = tid; g < P.NG; g += kCtaThreads) clear_slot(&gp[g], kSlotEmpty);
@@ -1591,7 +1598,192 @@ __global__ void __launch_bounds__(kCtaThreads, 1) k_verify_slab(StepParams P) {
         slot_r = slot_r + 1 == nbuf ? 0 : slot_r + 1;
     }
     // Inverse CDFs, spread over the CTAs once every residual is in.
-    for (int b = c; b < P.B && !(P.dbg & 1); b += grid) slab_locate<T>(P, b, sh, gcache);
+    for (int b = c; b < P.B && !(P.dbg & 1); b += grid) locate_row<T, ACT_SOFTMAX>(P, b, sh, gcache);
+    if (P.trace && tid == 0) atomicMax(&P.trace[8 * P.B + 1], gtime());
+}
+
+
+// ---------------------------------------------------------------------------
+// K2s k_verify_sig<T>: the sigmoid variant for batches the cluster path cannot
+// hold.  The paper's approximation needs no row statistics
+// (section 3.2.2), so one launch streams each batch row's needed row once:
+//   1. every warp decides its batch rows from the gathered logits alone
+//      (decide_gather: tau in fp64, first rejection) and publishes the
+//      decision slots -- while the first tiles already stream in;
+//   2. persistent CTAs take tiles (b, j) = elements [j*TE, (j+1)*TE) in a
+//      static round-robin; the bonus row's tile (the likely case: sigmoid
+//      acceptance is ~1 at the bench bounds) is copied into a shared-memory
+//      ring nbuf - 1 tiles ahead by cp.async, independent of the decision; a
+//      rejected row reads its pair from global instead.  Each warp reduces
+//      512-element granules (MUFU ex2 + rcp sigmoid, fp32 lanes, fp64 warp
+//      sum) into the granule slots;
+//   3. once every tile is in, CTA c runs the inverse CDF of rows c, c + grid,
+//      ... (locate: fp64 granule prefix, exact fp64 element scan).
+// One TMA bulk copy (cp.async.bulk, completion on the slot's mbarrier) of the
+// 16-byte-aligned superset of tile j of b's bonus row; thread 0 only.
+template <typename T>
+__device__ __forceinline__ void sig_issue(const StepParams& P, int b, int j, uint8_t* buf, uint64_t* bar) {
+    constexpr int VEC = Elem<T>::VEC;
+    const int TE = P.sg_te;
+    const T* row = p_row<T>(P, b, P.G) + (size_t)j * TE;
+    const uintptr_t g = reinterpret_cast<uintptr_t>(row);
+    const int shift = (int)((g & 15) / sizeof(T));
+    const int len = min(TE, P.V - j * TE);
+    const uint32_t bytes = (uint32_t)((shift + len + VEC - 1) / VEC) * 16u;
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // the slot's previous reads came first
+    mbar_arrive_expect_tx(bar, bytes);
+    bulk_g2s(buf, reinterpret_cast<const void*>(g & ~uintptr_t(15)), bytes, bar);
+}
+
+// Bonus-row granules of tile j (staged in shared memory at element offset
+// `shift`): warp w reduces granules w, w + 8, ...  Per element one FFMA for
+// -(z - alpha) / width * log2(e), MUFU ex2, one add, MUFU rcp, one add (fp32
+// lanes of 16 terms), then an fp64 warp sum -- the two granules' chains
+// interleaved.  Aligned full granules read 128-bit vectors.
+template <typename T, int ACT>
+__device__ __forceinline__ void sig_bonus_granules(const StepParams& P, int b, int j, const T* tb, int shift) {
+    constexpr int VEC = Elem<T>::VEC;
+    constexpr int NVL = kGW / VEC / 32;  // 16-byte vectors per lane per granule (4 fp32, 2 bf16)
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int GPT = P.sg_te / kGW;
+    const float sc = (float)(-1.4426950408889634 / P.width);
+    const float off = (float)(P.alpha * 1.4426950408889634 / P.width);
+    for (int t0 = warp; t0 < GPT; t0 += 2 * kWarps) {
+        double acc[2] = {0.0, 0.0};  // lane partials (fp32 chains of 16 terms)
+        int gg[2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int t = t0 + h * kWarps;
+            const int g = j * GPT + t;
+            gg[h] = t < GPT && g < P.NG ? g : -1;
+            if (gg[h] < 0) continue;
+            const int n = min(kGW, P.V - g * kGW);
+            const T* base = tb + shift + t * kGW;
+            if (ACT == ACT_SIGMOID && shift == 0 && n == kGW) {
+                const uint4* v = reinterpret_cast<const uint4*>(base) + lane;
+                float a = 0.f;
+#pragma unroll
+                for (int i = 0; i < NVL; ++i) {
+                    float x[VEC];
+                    unpack(v[32 * i], x);
+#pragma unroll
+                    for (int e = 0; e < VEC; ++e) {
+                        const float ex = ex2f(fmaf(x[e], sc, off));
+                        float r;
+                        asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(1.0f + ex));
+                        a += r;
+                    }
+                }
+                acc[h] = a;
+            } else {  // misaligned / short granule: the generic path (already warp-summed)
+                GranuleData<T> D;
+                Decision d{};
+                d.mode = MODE_BONUS;
+                granule_load<T, true>(P, b, g, d, D, base, base);
+                const double gs = granule_reduce<T, ACT>(P, d, D).y;
+                acc[h] = lane == 0 ? gs : 0.0;
+            }
+        }
+        double s0 = acc[0], s1 = acc[1];  // fixed-order fp64 warp sums, both chains interleaved
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            s0 += __shfl_xor_sync(kFull, s0, o);
+            s1 += __shfl_xor_sync(kFull, s1, o);
+        }
+        if (lane == 0) {
+            if (gg[0] >= 0) st_slot(&P.gpart[(size_t)b * P.NG + gg[0]], make_double2(0.0, s0));
+            if (gg[1] >= 0) st_slot(&P.gpart[(size_t)b * P.NG + gg[1]], make_double2(0.0, s1));
+        }
+    }
+}
+
+template <typename T, int ACT>
+__global__ void __launch_bounds__(kCtaThreads, 2) k_verify_sig(StepParams P) {
+    __shared__ Shared sh;
+    extern __shared__ __align__(128) uint8_t sig_smem[];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int TE = P.sg_te, GPT = TE / kGW, NT = P.sg_nt, nbuf = P.sg_nbuf;
+    pdl_enter();
+    const int grid = gridDim.x, c = blockIdx.x;
+    const int NU = P.B * NT;
+    const int nsteps = c < NU ? (NU - c + grid - 1) / grid : 0;
+    const bool spec = P.PS == P.G + 1;  // a bonus row exists: stream it speculatively
+    auto bufp = [&](int slot) { return sig_smem + (size_t)slot * P.sg_tb; };
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sig_smem + (size_t)nbuf * P.sg_tb);  // one mbarrier per slot
+    double2* gcache = reinterpret_cast<double2*>(sig_smem + (size_t)nbuf * P.sg_tb + 64);  // locate's granule cache
+    if (P.trace && c == 0 && tid == 0) trace(P, 8 * P.B);
+    if (tid == 0) {
+        for (int i = 0; i < nbuf; ++i) mbar_init(&bars[i], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    // 1. decisions from the gathers (warp per batch row), before the tile
+    // stream starts: the two dependent round trips (ids, then logits) see an
+    // idle memory system.
+    for (int b = c * kWarps + warp; b < P.B; b += grid * kWarps) {
+        Decision d;
+        decide_gather<T, ACT>(P, b, true, d);
+        __syncwarp();
+        if (lane == 0) {
+            publish_decision(P, b, d);
+            trace(P, 8 * b + 2);
+        }
+    }
+    if (tid == 0) {
+        for (int k = 0; k < nbuf - 1 && spec && k < nsteps; ++k) {
+            const int u = c + k * grid, b = u / NT;
+            sig_issue<T>(P, b, u - b * NT, bufp(k), &bars[k]);
+        }
+    }
+    __syncthreads();  // barriers initialized
+    // 2. tiles.  Thread 0 keeps the decision words of the next kDecAhead
+    // tiles in flight (a loaded L2 round trip is ~2 us, a tile ~0.7 us).
+    constexpr int kDecAhead = 4;
+    DecRaw pre[kDecAhead];
+    if (tid == 0) {
+#pragma unroll
+        for (int i = 0; i < kDecAhead; ++i)
+            if (i < nsteps) dec_issue(P, (c + i * grid) / NT, pre[i]);
+    }
+    int slot_k = 0, slot_i = (nbuf - 1) % nbuf;
+    for (int k = 0; k < nsteps; ++k) {
+        if (tid == 0 && spec && k + nbuf - 1 < nsteps) {
+            const int u = c + (k + nbuf - 1) * grid, b = u / NT;
+            sig_issue<T>(P, b, u - b * NT, bufp(slot_i), &bars[slot_i]);
+        }
+        const int u = c + k * grid, b = u / NT, j = u - b * NT;
+        if (tid == 0) {
+            Decision d;
+            if (!dec_decode(pre[0], d)) d = wait_decision(P, b);
+            sh.dec = d;
+#pragma unroll
+            for (int i = 0; i + 1 < kDecAhead; ++i) pre[i] = pre[i + 1];
+            if (k + kDecAhead < nsteps) dec_issue(P, (u + kDecAhead * grid) / NT, pre[kDecAhead - 1]);
+        }
+        __syncthreads();  // decision in sh.dec
+        const Decision d = sh.dec;
+        if (spec) mbar_wait(&bars[slot_k], (uint32_t)((k / nbuf) & 1));  // tile k has landed
+        const T* tb = reinterpret_cast<const T*>(bufp(slot_k));
+        const int shift = (int)((reinterpret_cast<uintptr_t>(p_row<T>(P, b, P.G) + (size_t)j * TE) & 15) / sizeof(T));
+        if (d.mode == MODE_BONUS) {
+            sig_bonus_granules<T, ACT>(P, b, j, tb, shift);
+        } else {
+            for (int t = warp; t < GPT; t += kWarps) {
+                const int g = j * GPT + t;
+                if (g >= P.NG) break;
+                double2 out = make_double2(0.0, 0.0);
+                if (d.mode == MODE_REJECT) granule<T, ACT>(P, b, g, d, &out);
+                if (lane == 0) st_slot(&P.gpart[(size_t)b * P.NG + g], out);
+            }
+        }
+        if (j == 0 && tid == 0) trace(P, 8 * b + 3);
+        __syncthreads();  // buffer of step k is free
+        slot_k = slot_k + 1 == nbuf ? 0 : slot_k + 1;
+        slot_i = slot_i + 1 == nbuf ? 0 : slot_i + 1;
+    }
+    // 3. inverse CDFs once every tile is in (a locate inside the stream stalls
+    // its CTA for ~4 us of dependent round trips, and a locate waiting on a CTA
+    // busy with its own chains the stalls: measured slower either way).
+    for (int b = c; b < P.B; b += grid) locate_row<T, ACT>(P, b, sh, gcache);
     if (P.trace && tid == 0) atomicMax(&P.trace[8 * P.B + 1], gtime());
 }
 
@@ -2720,6 +2912,64 @@ static void launch_slab_t(const StepParams& P, const Launch& L) {
     L.end(h);
 }
 
+// Sigmoid-stream geometry (sg_on 0 = not applicable): tiles of TE elements
+// (32 KB of one row), a ring of nbuf tiles per CTA, one CTA per SM.
+template <typename T, int ACT>
+static bool plan_sig_t(StepParams& P) {
+    P.sg_on = 0;
+    if (P.sample_mode) return false;
+    const int TE = 32768 / (int)sizeof(T);  // multiple of kGW * kWarps
+    const int tb = ((TE + 2 * (16 / (int)sizeof(T))) * (int)sizeof(T) + 127) & ~127;
+    // Two CTAs per SM (16 warps to hide the per-element MUFU chains), each a
+    // ring of two 32 KB tiles (three measured no faster) plus the locate's
+    // granule cache.
+    static const int nb_env = knob("SSV_SIG_NBUF", 0);
+    const int nbuf = nb_env > 1 ? nb_env : 2;
+    const int smem = nbuf * tb + 64 + std::min(P.NG, kLocCap) * (int)sizeof(double2);
+    if (smem > kSlabSmemMax || nbuf < 2) return false;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_verify_sig<T, ACT>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSlabSmemMax);
+        attr = true;
+    }
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_verify_sig<T, ACT>, kCtaThreads, smem);
+    if (per_sm < 1) return false;
+    P.sg_on = 1;
+    P.sg_te = TE;
+    P.sg_nt = (P.V + TE - 1) / TE;
+    P.sg_nbuf = nbuf;
+    P.sg_tb = tb;
+    P.sg_smem = smem;
+    P.sg_grid = sm_count() * per_sm;
+    return true;
+}
+
+bool plan_sig(int dtype, int act, StepParams& P) {
+    P.sg_on = 0;
+    if (act != ACT_SIGMOID) return false;
+    if (dtype == DT_F32) return plan_sig_t<float, ACT_SIGMOID>(P);
+    if (dtype == DT_BF16) return plan_sig_t<__nv_bfloat16, ACT_SIGMOID>(P);
+    return false;
+}
+
+template <typename T, int ACT>
+static void launch_sig_t(const StepParams& P, const Launch& L) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)P.sg_grid, 1, 1);
+    cfg.blockDim = dim3(kCtaThreads, 1, 1);
+    cfg.dynamicSmemBytes = P.sg_smem;
+    cfg.stream = L.st;
+    cudaLaunchAttribute at[2];
+    at[0].id = cudaLaunchAttributeCooperative;  // the locates wait on every CTA's tiles
+    at[0].val.cooperative = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1 + pdl_attr(at[1]);
+    const int h = L.begin(KID_VERIFY);
+    cudaLaunchKernelEx(&cfg, k_verify_sig<T, ACT>, P);
+    L.end(h);
+}
+
 template <typename T, int ACT>
 static void launch_mat_t(const StepParams& P, void* p, void* q, void* r, const Launch& L) {
     const int h = L.begin(KID_MATERIALIZE);
@@ -2733,6 +2983,9 @@ static void launch_step_t(const StepParams& P, const Launch& L) {
         if (P.cl_size > 0) return launch_cluster_t<T, ACT>(P, L);
         if constexpr (ACT == ACT_SOFTMAX) {
             if (P.sl_on) return launch_slab_t<T>(P, L);
+        }
+        if constexpr (ACT == ACT_SIGMOID) {
+            if (P.sg_on) return launch_sig_t<T, ACT>(P, L);
         }
     }
     launch_verify_t<T, ACT>(P, L);

@@ -83,6 +83,10 @@ struct StepParams {
     // 2*gamma drafted rows of batch row b, held in a shared-memory buffer until
     // b's decision is known.
     int sl_on, sl_ns, sl_nbuf, sl_dp, sl_lag, sl_ub, sl_smem, sl_grid, sl_dbg;
+    // Sigmoid-stream path (large batches, see k_verify_sig): tiles of sg_te
+    // elements of each batch row's needed row, sg_nt per row, a ring of sg_nbuf
+    // tile buffers of sg_tb bytes per CTA.
+    int sg_on, sg_te, sg_nt, sg_nbuf, sg_tb, sg_smem, sg_grid;
     int dbg;  // experiment bits (SSV_DBG_MODE), 0 in production
     double alpha, width;
     int sample_mode;     // sample softmax(z_p row b) with u[b] (draft sampling)
@@ -151,6 +155,7 @@ void plan_geometry(int dtype, int act, StepParams& P);
 void launch_fill_slots(void* p, size_t n_u64, cudaStream_t st);
 bool plan_cluster(int dtype, int act, StepParams& P, bool allow_resident = true);  // small-batch cluster path (sets cl_*)
 bool plan_slab(int dtype, int act, StepParams& P);  // exact, large batches (sets sl_*)
+bool plan_sig(int dtype, int act, StepParams& P);   // sigmoid, large batches (sets sg_*)
 int trace_slots(const StepParams& P);
 void launch_verify(int dtype, int act, const StepParams& P, void* outp, void* outq, void* outr,
                    const Launch& L);

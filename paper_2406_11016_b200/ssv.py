@@ -221,7 +221,7 @@ class Verifier:
         """The plan the last verify call launched (ssv_last_plan)."""
         info = (C.c_int32 * 6)()
         self._check(self.lib.ssv_last_plan(self.ctx, info, 6), "ssv_last_plan")
-        kind = {0: "streaming", 1: "cluster_resident", 2: "cluster_ring", 3: "slab"}[info[0]]
+        kind = {0: "streaming", 1: "cluster_resident", 2: "cluster_ring", 3: "slab", 4: "sigmoid_stream"}[info[0]]
         return {"kernel": kind, "cluster_size": info[1], "threads": info[2], "slots": info[3], "rows": info[4],
                 "pieces": info[5]}
 
