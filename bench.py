@@ -398,6 +398,67 @@ def run_reference_arm(args):
     print(json.dumps(line), flush=True)
 
 
+# ----------------------------------------------------------------------------- config 5 sweep
+SWEEP_GAMMAS = (1, 2, 4, 8, 16)
+SWEEP_BATCHES = (1, 8, 64, 256, 1024)
+SWEEP_VOCABS = (32000, 51865, 151936)
+SWEEP_COLS = ["gamma", "B", "V", "dtype", "variant", "plan", "gpu_us_per_step", "gpu_tokens_per_s",
+              "algorithmic_bytes", "gbs", "frac", "cpu_tokens_per_s", "cpu_rows", "cpu_cores", "gpu_over_cpu"]
+
+
+def run_sweep(a):
+    """--sweep: BASELINE.json config 5 on one GPU -- the gamma x B x V grid,
+    GPU verified drafted tokens/s and roofline fraction (device-resident
+    ssv_make_bench_inputs logits, inputs rotated past L2, graph-replayed steps,
+    CUDA events) beside the reference's CPU path on the same recipe (cpu_baseline
+    leg: oracle/_ref on a row subsample of tools/benchgen.c rows, all host cores,
+    per-row rate; rows are independent, verify_reference.cpp:87-109).  The
+    reference's own grid harness is bench.cpp:155-210.  One CSV row per point."""
+    import csv
+
+    import torch
+
+    from oracle.oracle import ref_available
+    from paper_2406_11016_b200 import Verifier
+    from tools import benchgen
+
+    v = Verifier(0)
+    peak, _ = load_peaks()
+    cores = os.cpu_count() or 1
+    out = open(a.sweep_out, "w", newline="") if a.sweep_out else sys.stdout
+    w = csv.DictWriter(out, fieldnames=SWEEP_COLS)
+    w.writeheader()
+    for V in map(int, a.sweep_vocabs.split(",")):
+        for g in map(int, a.sweep_gammas.split(",")):
+            for B in map(int, a.sweep_batches.split(",")):
+                key = f"c5-{g}-{B}-{V}"
+                WORKLOADS[key] = (key, B, g, V, a.sweep_dtype)
+                wl = Workload(v, key, 0, 1, a.variant, host_gen=False)
+                K = 20 if wl.set_bytes > 2e9 else 100
+                m = measure_device(v, wl, K, 5, 1)
+                res = m["result"].numpy()
+                kb, _ = algorithmic_bytes(a.variant, B, g, V, wl.s, res.accepted_len)
+                us = m["ms_per_step"] * 1e3
+                plan = v.last_plan["kernel"]
+                del wl
+                torch.cuda.empty_cache()
+                row = {"gamma": g, "B": B, "V": V, "dtype": a.sweep_dtype, "variant": a.variant, "plan": plan,
+                       "gpu_us_per_step": round(us, 2), "gpu_tokens_per_s": round(B * g / (us * 1e-6)),
+                       "algorithmic_bytes": kb, "gbs": round(kb / us / 1e3, 1), "frac": round(kb / us / 1e3 / peak, 3)}
+                if ref_available():
+                    rows = max(1, min(B, 4))
+                    zp, zq, ids, u = benchgen.make_bench_batch(1, rows, g, V, a.sweep_dtype)
+                    val, _, r_used, _ = time_reference(benchgen.widen(zp, a.sweep_dtype),
+                                                       benchgen.widen(zq, a.sweep_dtype), ids, u, a.variant,
+                                                       a.sweep_cpu_budget, cores)
+                    row.update(cpu_tokens_per_s=round(val), cpu_rows=r_used, cpu_cores=cores,
+                               gpu_over_cpu=round(row["gpu_tokens_per_s"] / val, 1))
+                w.writerow(row)
+                out.flush()
+    if a.sweep_out:
+        out.close()
+
+
 # ----------------------------------------------------------------------------- main
 EXTRAS = (("c4", "sigmoid"), ("c4bf16", "exact"), ("c4shard", "exact"), ("c3", "exact"), ("c3bf16", "exact"),
           ("c3", "sigmoid"), ("c2", "exact"), ("c2", "sigmoid"), ("c1", "exact"), ("c1", "sigmoid"))
@@ -431,7 +492,16 @@ def main():
     ap.add_argument("--no-extra", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--sweep", action="store_true", help="BASELINE config 5 grid on one GPU (CSV), then exit")
+    ap.add_argument("--sweep-out", default="")
+    ap.add_argument("--sweep-dtype", default="f32", choices=["f32", "bf16"])
+    ap.add_argument("--sweep-cpu-budget", type=float, default=1.0, help="reference CPU seconds per point")
+    ap.add_argument("--sweep-gammas", default=",".join(map(str, SWEEP_GAMMAS)))
+    ap.add_argument("--sweep-batches", default=",".join(map(str, SWEEP_BATCHES)))
+    ap.add_argument("--sweep-vocabs", default=",".join(map(str, SWEEP_VOCABS)))
     args = ap.parse_args()
+    if args.sweep:
+        return run_sweep(args)
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")
     if args.impl == "reference":
@@ -442,22 +512,33 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
+    # One rank per GPU (NCCL carries only the barrier and the max-over-ranks
+    # time).  With fewer GPUs than ranks (a one-GPU box exercising the N > 1
+    # path) the ranks share devices round-robin and the host-side plumbing runs
+    # on gloo: that run checks the sharded flow, it is not a scaling number.
+    ndev = torch.cuda.device_count()
+    dev_index = local % max(1, ndev)
+    shared = world > ndev
+    torch.cuda.set_device(dev_index)
+    backend = "gloo" if shared else "nccl"
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if shared:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev_index))
     from paper_2406_11016_b200 import Verifier
     from paper_2406_11016_b200.shard import allmax as _allmax
 
     def allmax(x):
-        return _allmax(x, device="cuda")
+        return _allmax(x, device="cpu" if shared else "cuda")
 
-    v = Verifier(local)
+    v = Verifier(dev_index)
     peak, peak_src = load_peaks()
     desc, Bg, gamma, V, storage = WORKLOADS[args.workload]
     wl = Workload(v, args.workload, rank, world, args.variant)
-    sampler = ClockSampler(local)
+    sampler = ClockSampler(dev_index)
     m = measure_device(v, wl, args.steps, args.warmup, world, sampler)
     res = m["result"].numpy()
     k_bytes, A = algorithmic_bytes(args.variant, wl.B, gamma, V, wl.s, res.accepted_len)
@@ -495,6 +576,9 @@ def main():
             "l2": f"inputs rotate over {wl.R} copies ({wl.R * wl.set_bytes / 1e6:.0f} MB > 3x L2 "
                   f"{wl.l2 / 1e6:.0f} MB): every step reads HBM",
             "timing": "K steps replayed as one CUDA graph, CUDA events on the launching stream, max over ranks",
+            "process_group": backend if world > 1 else None,
+            "devices": (f"{world} ranks share {ndev} GPU(s): a path check of the sharded flow, not a scaling "
+                        "measurement") if shared else f"one GPU per rank ({world})",
         },
         "gpu_launches": args.steps * m["launches_per_step"],
         "accepted_all_rows": A,

@@ -243,7 +243,7 @@ class Ref(_Base):
         L.ref_make_bench_inputs.argtypes = [C.c_uint64, C.c_int, C.c_int, _dp, _dp, _ip, _dp]
         L.ref_make_model_pair.argtypes = [C.c_uint64, C.c_int, C.c_double, C.c_double, _dp, _dp]
         L.ref_decode.argtypes = [_dp, _dp, C.c_int, _ip, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_uint64,
-                                 C.c_int, C.c_double, C.c_double, _ip, _ip, C.POINTER(C.c_int)]
+                                 C.c_int, C.c_double, C.c_double, C.c_int, _ip, _ip, C.POINTER(C.c_int)]
         L.ref_time_backend.argtypes = [C.c_int] + vargs + [
             C.c_double, C.c_double, C.c_int, C.c_uint, C.c_int, C.c_int, _dp, C.POINTER(_Out)]
 
@@ -306,7 +306,7 @@ class Ref(_Base):
         return t, d
 
     def decode(self, target, draft, prompt, max_len, gamma=5, min_gamma=1, max_gamma=64, seed=0,
-               backend="reference", alpha=-1e3, beta=1e3):
+               backend="reference", alpha=-1e3, beta=1e3, emulate_half=False):
         """decode.cpp:45-159 (Backend reference / fused / sigmoid) on the given tables."""
         V = target.shape[0]
         target = np.ascontiguousarray(target, np.float64)
@@ -317,6 +317,6 @@ class Ref(_Base):
         steps = C.c_int(0)
         code = {"reference": 0, "fused": 1, "sigmoid": 2}[backend]
         if self.lib.ref_decode(target, draft, V, prompt, prompt.size, max_len, gamma, min_gamma, max_gamma, seed,
-                               code, alpha, beta, tokens, hist, C.byref(steps)):
+                               code, alpha, beta, int(emulate_half), tokens, hist, C.byref(steps)):
             raise ValueError("reference: " + self.lib.ref_last_error().decode())
         return tokens, hist[:steps.value]

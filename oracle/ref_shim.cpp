@@ -271,11 +271,11 @@ int ref_make_model_pair(uint64_t seed, int V, double divergence, double logit_sc
 }
 
 // decode.cpp:45-159 on given tables (temperature 1).  backend 0 reference,
-// 1 fused, 2 sigmoid.  Writes max_len tokens and the gamma history (max_len
+// 1 fused, 2 sigmoid (emulate_half: the binary16 emulation, as ablate.cpp:66-75 runs it).  Writes max_len tokens and the gamma history (max_len
 // entries at most); returns the step count through *steps.
 int ref_decode(const double* target, const double* draft, int V, const int32_t* prompt, int prompt_len,
                int max_len, int gamma0, int min_gamma, int max_gamma, uint64_t seed, int backend, double alpha,
-               double beta, int32_t* tokens, int32_t* gamma_hist, int* steps) {
+               double beta, int emulate_half, int32_t* tokens, int32_t* gamma_hist, int* steps) {
     return guarded([&] {
         ToyModel t, d;
         t.vocab_size = d.vocab_size = (size_t)V;
@@ -287,6 +287,7 @@ int ref_decode(const double* target, const double* draft, int V, const int32_t* 
         cfg.gamma = GammaState{gamma0, min_gamma, max_gamma};
         cfg.workers = 2;
         cfg.bounds = ScaleBounds{alpha, beta};
+        cfg.emulate_half = emulate_half != 0;
         cfg.seed = seed;
         const DecodeOutput out = decode(t, d, std::span<const int32_t>(prompt, (size_t)prompt_len), cfg);
         std::memcpy(tokens, out.tokens.data(), sizeof(int32_t) * out.tokens.size());

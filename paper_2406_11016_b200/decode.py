@@ -59,13 +59,18 @@ class DecodeStats:
     total_accepted: int = 0
     gamma_history: list = field(default_factory=list)
     all_accepted_history: list = field(default_factory=list)
+    verify_ns: list = field(default_factory=list)  # per step: the verify call incl. its result read (decode.cpp:121-135)
 
 
 def decode(verifier, target, draft, prompt, max_len: int, gamma: int = 5, min_gamma: int = 1,
            max_gamma: int = 64, seed: int = 0, variant: str = "exact", alpha: float = -1e3,
-           beta: float = 1e3):
+           beta: float = 1e3, emulate_half: bool = False):
     """decode.cpp:45-159 on the CUDA backend.  `target` / `draft` are [V, V]
-    CUDA tensors (fp32 or bf16 logits); returns (tokens, DecodeStats)."""
+    CUDA tensors (fp32 or bf16 logits); returns (tokens, DecodeStats).
+    emulate_half: the sigmoid variant's binary16 emulation (DecodeConfig::
+    emulate_half, decode.hpp:35), as the scale ablation runs it."""
+    import time
+
     import torch
 
     if len(prompt) == 0:
@@ -97,11 +102,13 @@ def decode(verifier, target, draft, prompt, max_len: int, gamma: int = 5, min_ga
         z_p = target.index_select(0, rows).unsqueeze(0)
         z_q = draft.index_select(0, rows[:g]).unsqueeze(0)
         ids = torch.tensor([drafted], dtype=torch.int32, device=dev)
+        t0 = time.perf_counter_ns()
         if variant == "exact":
             r = verifier.verify_exact(z_p, z_q, ids, u)
         else:
-            r = verifier.verify_sigmoid(z_p, z_q, ids, u, alpha, beta)
+            r = verifier.verify_sigmoid(z_p, z_q, ids, u, alpha, beta, emulate_half=emulate_half)
         accepted = int(r.accepted_len[0].item())
+        stats.verify_ns.append(time.perf_counter_ns() - t0)
         tokens.extend(drafted[:accepted])
         tokens.append(int(r.final_token[0].item()))
         all_acc = accepted == g

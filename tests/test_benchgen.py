@@ -27,3 +27,14 @@ def test_benchgen_bench_shape_rows(ref):
         assert np.array_equal(zp[0], rzp.astype(np.float32))
         assert np.array_equal(zq[0], rzq.astype(np.float32))
         assert np.array_equal(ids[0], rids) and np.array_equal(u[0], ru)
+
+
+def test_model_pair_matches_reference(ref):
+    """tools/benchgen.c make_model_pair == the compiled reference's
+    (toy_model.cpp:16-42), bit for bit, for both ablation profiles."""
+    from tools import benchgen
+
+    for seed, V, div, scale in ((1, 127, 3000.0, 8000.0), (5, 257, 2000.0, 8000.0), (3, 64, 0.5, 4.0)):
+        t, d = benchgen.make_model_pair(seed, V, div, scale)
+        rt, rd = ref.make_model_pair(seed, V, div, scale)
+        assert np.array_equal(t, rt) and np.array_equal(d, rd)

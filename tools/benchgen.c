@@ -143,3 +143,16 @@ int bg_make_bench_batch(uint64_t seed, int B, int gamma, int V, int dtype, int t
     free(jobs);
     return 0;
 }
+
+/* toy_model.cpp:16-42 make_model_pair: target table = logit_scale * N(0,1)
+ * from stream `seed`, draft = target + divergence * N(0,1) from stream
+ * seed ^ 0xd1f (row-major [V][V], doubles).  The ablation's input tables. */
+int bg_make_model_pair(uint64_t seed, int V, double divergence, double logit_scale, double* target, double* draft) {
+    if (V < 2 || divergence < 0.0) return 1;
+    const size_t n = (size_t)V * (size_t)V;
+    bg_rng t = {seed, 0};
+    for (size_t i = 0; i < n; ++i) target[i] = logit_scale * bg_normal(&t);
+    bg_rng d = {seed ^ 0xd1fu, 0};
+    for (size_t i = 0; i < n; ++i) draft[i] = target[i] + divergence * bg_normal(&d);
+    return 0;
+}

@@ -30,6 +30,7 @@ def lib():
         L = C.CDLL(LIB)
         L.bg_make_bench_batch.argtypes = [C.c_uint64, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_void_p,
                                           C.c_void_p, C.c_void_p, C.c_void_p]
+        L.bg_make_model_pair.argtypes = [C.c_uint64, C.c_int, C.c_double, C.c_double, C.c_void_p, C.c_void_p]
         _lib = L
     return _lib
 
@@ -58,3 +59,13 @@ def widen(x, storage):
     if storage == "bf16":
         return (x.astype(np.uint32) << 16).view(np.float32).astype(np.float64)
     return x.astype(np.float64)
+
+
+def make_model_pair(seed, V, divergence, logit_scale=4.0):
+    """toy_model.cpp:16-42: the (target, draft) order-1 Markov logit tables,
+    [V, V] float64 (the ablation's and the decode loop's inputs)."""
+    t = np.empty((V, V), np.float64)
+    d = np.empty((V, V), np.float64)
+    if lib().bg_make_model_pair(seed, V, divergence, logit_scale, t.ctypes.data, d.ctypes.data):
+        raise ValueError("make_model_pair: vocab_size must be >= 2 and divergence >= 0")
+    return t, d

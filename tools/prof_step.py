@@ -24,4 +24,10 @@ zp, zq, ids, u = v.make_bench_inputs(1, a.B, a.gamma, a.V, dt)
 for _ in range(a.iters):
     r = v.verify_exact(zp, zq, ids, u) if a.variant == "exact" else v.verify_sigmoid(zp, zq, ids, u)
 torch.cuda.synchronize()
-print(r.accepted_len.tolist(), r.final_token.tolist())
+import json  # noqa: E402
+
+import bench  # noqa: E402
+
+kb, A = bench.algorithmic_bytes(a.variant, a.B, a.gamma, a.V, 4 if a.dtype == "f32" else 2, r.accepted_len.cpu().numpy())
+print("PROF_STEP " + json.dumps({"algorithmic_bytes": kb, "accepted_all_rows": A, "plan": v.last_plan,
+                                 "final_token": r.final_token.tolist()[:8]}))
