@@ -1062,6 +1062,7 @@ __device__ void locate(const StepParams& P, int b, const Decision& d, Shared& sh
                 a1 += v.x;
                 a2 += v.y;
             }
+            if (P.trace && b == 0 && lane == 0) P.trace[8 * P.B + 23] = (unsigned long long)(clock64() - cyc0);
             const double i1 = warp_scan_incl(a1), i2 = warp_scan_incl(a2);
             const double sa = __shfl_sync(kFull, i1, 31), sp = __shfl_sync(kFull, i2, 31);
             useA = sa > kZeroEps;  // verify_reference.cpp:57-62
@@ -1098,6 +1099,7 @@ __device__ void locate(const StepParams& P, int b, const Decision& d, Shared& sh
                 if (P.rden) P.rden[b] = 0.0;
             }
         }
+        if (P.trace && b == 0 && lane == 0) P.trace[8 * P.B + 24] = (unsigned long long)(clock64() - cyc0);
         const double norm = d.mode != MODE_REJECT && ACT == ACT_SOFTMAX ? gS : denom;
         thr = u * norm;
         int hit = 0x7fffffff;

@@ -6,7 +6,7 @@ mkdir -p $OUT
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,memory.total --format=csv > $OUT/gpu.txt 2>&1
 timeout 900 python bench.py > $OUT/bench.json 2> $OUT/bench.err
 timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
-   -k regex:k_verify -c 200 --csv --log-file $OUT/launches.csv python bench.py --steps 30 --warmup 3 --no-extra --no-cpu > $OUT/ncu_bench.out 2>&1
+   -k regex:k_verify -c 200 --csv --log-file $OUT/launches.csv python bench.py --steps 30 --warmup 3 --no-extra --no-cpu --no-e2e > $OUT/ncu_bench.out 2>&1
 for cfg in "8 5 51865 f32 exact c2" "256 8 151936 f32 exact c4" "64 8 32000 f32 exact c3" "8 5 51865 f32 sigmoid c2" "256 8 151936 f32 sigmoid c4" "256 8 151936 bf16 exact c4bf16" "1 5 32000 f32 exact c1"; do
   set -- $cfg
   timeout 600 ncu --set full --import-source on --clock-control none -k regex:k_verify -s 3 -c 1 \

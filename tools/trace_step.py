@@ -56,7 +56,8 @@ if lo[3] > 0:
     f2 = lambda x: f"{(x - t0) / 1e3:.1f}" if x > 0 else "-"
     print(f"row-0 locate (us): enter {f2(lo[3])} level1-done {f2(lo[0])} level2-values {f2(lo[1])} end {f2(lo[2])}")
 if t[8 * a.B + 22] > 0:
-    print(f"row-0 locate level-1 on warp 0: {int(t[8 * a.B + 22])} cycles")
+    print(f"row-0 locate level-1 on warp 0: {int(t[8 * a.B + 22])} cycles (sums done {int(t[8 * a.B + 23])}, "
+          f"scans done {int(t[8 * a.B + 24])})")
 
 if os.environ.get("SSV_SLAB_TRACE"):
     ct = t[8 * a.B + 26: 8 * a.B + 26 + 148 * 8].reshape(148, 8)
