@@ -364,6 +364,7 @@ __device__ void item_A(const StepParams& P, int b, int idx, const ItemRef& nxt, 
     const int shift = cur.shift, tail = cur.tail, nvec_row = cur.nvec_row;
     using A = typename Elem<T>::acc;
     A m = -FLT_MAX, mn = FLT_MAX;
+    uint32_t mnp = 0x7f7f7f7fu;  // bf16: packed running minimum (largest finite pair)
     if constexpr (sizeof(T) == 8) {
         m = -DBL_MAX;
         mn = DBL_MAX;
@@ -423,8 +424,24 @@ __device__ void item_A(const StepParams& P, int b, int idx, const ItemRef& nxt, 
             }
         } else {
             float cm = -FLT_MAX;
+            if constexpr (sizeof(T) == 2) {
+                // bf16: packed VHMNMX over the chunk's words (4 per vector), one
+                // running packed minimum for the whole run, a single widening of
+                // the chunk maximum -- ~0.5 fewer instructions per element than
+                // widening per vector.
+                uint32_t mx = AStat<T>::max2(AStat<T>::max2(w[0].x, w[0].y), AStat<T>::max2(w[0].z, w[0].w));
+                uint32_t mi = AStat<T>::min2(AStat<T>::min2(w[0].x, w[0].y), AStat<T>::min2(w[0].z, w[0].w));
 #pragma unroll
-            for (int j = 0; j < kAVec; ++j) AStat<T>::minmax(w[j], cm, mn);
+                for (int j = 1; j < kAVec; ++j) {
+                    mx = AStat<T>::max2(mx, AStat<T>::max2(AStat<T>::max2(w[j].x, w[j].y), AStat<T>::max2(w[j].z, w[j].w)));
+                    mi = AStat<T>::min2(mi, AStat<T>::min2(AStat<T>::min2(w[j].x, w[j].y), AStat<T>::min2(w[j].z, w[j].w)));
+                }
+                cm = fmaxf(__uint_as_float(mx << 16), __uint_as_float(mx & 0xffff0000u));
+                mnp = AStat<T>::min2(mnp, mi);
+            } else {
+#pragma unroll
+                for (int j = 0; j < kAVec; ++j) AStat<T>::minmax(w[j], cm, mn);
+            }
             // Warp-uniform running max: when the warp's max grows (rarely, after
             // the first chunks) every lane rescales its fp64 sum by the same
             // factor, and the end-of-run fold needs no exp at all.
@@ -450,6 +467,7 @@ __device__ void item_A(const StepParams& P, int b, int idx, const ItemRef& nxt, 
         }
     }
     as.next_pre = nxt_issued;
+    if constexpr (sizeof(T) == 2) mn = fmin3f_nan(FLT_MAX, __uint_as_float(mnp << 16), __uint_as_float(mnp & 0xffff0000u));
     // -inf or NaN logit (require_finite, dist.cpp:27-36; the running minimum
     // propagates NaN even where the max and the sum skip it); +inf surfaces in the sum
     if (__any_sync(kFull, !isfinite(mn)) && lane == 0) flag(P, SSV_STATUS_NONFINITE);
