@@ -159,6 +159,8 @@ def algorithmic_bytes(variant, B, gamma, V, s, accepted_len):
     small = 4 * B * gamma + 8 * B * (gamma + 1) + (17 + 8 * gamma) * B
     if variant == "exact":
         return s * V * (2 * gamma * B + A) + small, A
+    if variant == "exact_grids":  # + the p, q and residual grids written once (fp32)
+        return s * V * (2 * gamma * B + A) + 4 * V * B * (3 * gamma + 1) + small, A
     return s * V * (A + 2 * R) + 2 * s * B * gamma + small, A
 
 
@@ -215,6 +217,10 @@ class Workload:
         zp, zq, ids, u = self.sets[k % self.R]
         if self.variant == "exact":
             return v.verify_exact(zp, zq, ids, u, out=out)
+        if self.variant == "exact_grids":  # the optional outputs: verify + the p / q / residual grids
+            from paper_2406_11016_b200 import SSV_WANT_P, SSV_WANT_Q, SSV_WANT_RESIDUAL
+
+            return v.verify_exact(zp, zq, ids, u, flags=SSV_WANT_P | SSV_WANT_Q | SSV_WANT_RESIDUAL, out=out)
         return v.verify_sigmoid(zp, zq, ids, u, -1e3, 1e3, out=out)
 
 
@@ -461,7 +467,8 @@ def run_sweep(a):
 
 # ----------------------------------------------------------------------------- main
 EXTRAS = (("c4", "sigmoid"), ("c4bf16", "exact"), ("c4shard", "exact"), ("c3", "exact"), ("c3bf16", "exact"),
-          ("c3", "sigmoid"), ("c2", "exact"), ("c2", "sigmoid"), ("c1", "exact"), ("c1", "sigmoid"))
+          ("c3", "sigmoid"), ("c2", "exact"), ("c2", "sigmoid"), ("c1", "exact"), ("c1", "sigmoid"),
+          ("c2", "exact_grids"), ("c4shard", "exact_grids"))
 
 
 def extra_line(v, key, variant, peak):

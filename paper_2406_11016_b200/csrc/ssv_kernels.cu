@@ -2386,17 +2386,31 @@ __global__ void __launch_bounds__(kThreads) k_materialize(StepParams P, void* ou
             if (is_sigmoid(ACT)) return sigmoid_fast((x - alpha) * invw);
             return x;
         };
-        const T* pr = p_row<T>(P, b, c);
-        const T* qr = is_pair ? q_row<T>(P, b, c) : nullptr;
-        O* op = outp ? reinterpret_cast<O*>(outp) + ((size_t)b * P.PS + c) * (size_t)V : nullptr;
-        O* oq = (outq && is_pair) ? reinterpret_cast<O*>(outq) + ((size_t)b * G + c) * (size_t)V : nullptr;
-        O* orr = (outr && is_pair) ? reinterpret_cast<O*>(outr) + ((size_t)b * G + c) * (size_t)V : nullptr;
-        for (int i = lo + threadIdx.x; i < hi; i += kThreads) {
-            const bool need_p = op || orr;
-            const A pv = need_p ? act(load_elem(pr + i), Mp, iSp) : (A)0;
+        const T* __restrict__ pr = p_row<T>(P, b, c);
+        const T* __restrict__ qr = is_pair ? q_row<T>(P, b, c) : nullptr;
+        O* __restrict__ op = outp ? reinterpret_cast<O*>(outp) + ((size_t)b * P.PS + c) * (size_t)V : nullptr;
+        O* __restrict__ oq = (outq && is_pair) ? reinterpret_cast<O*>(outq) + ((size_t)b * G + c) * (size_t)V : nullptr;
+        O* __restrict__ orr = (outr && is_pair) ? reinterpret_cast<O*>(outr) + ((size_t)b * G + c) * (size_t)V : nullptr;
+        const bool need_p = op || orr, need_q = is_pair && want_q;
+        // All of the segment's loads first (kMatSeg / kThreads per thread in
+        // flight), then the values and the stores: one memory latency per unit
+        // instead of one per element (the stores could alias the loads).
+        constexpr int EPT = kMatSeg / kThreads;
+        A xp[EPT], xq[EPT];
+#pragma unroll
+        for (int e = 0; e < EPT; ++e) {
+            const int i = lo + threadIdx.x + e * kThreads;
+            xp[e] = need_p && i < hi ? load_elem(pr + i) : (A)0;
+            xq[e] = need_q && i < hi ? load_elem(qr + i) : (A)0;
+        }
+#pragma unroll
+        for (int e = 0; e < EPT; ++e) {
+            const int i = lo + threadIdx.x + e * kThreads;
+            if (i >= hi) break;
+            const A pv = need_p ? act(xp[e], Mp, iSp) : (A)0;
             if (op) op[i] = (O)pv;
-            if (is_pair && want_q) {
-                const A qv = act(load_elem(qr + i), Mq, iSq);
+            if (need_q) {
+                const A qv = act(xq[e], Mq, iSq);
                 if (oq) oq[i] = (O)qv;
                 if (orr) orr[i] = (O)(pv - qv > (A)0 ? pv - qv : (A)0);
             }
