@@ -1764,23 +1764,27 @@ __global__ void __launch_bounds__(kCtaThreads, 2) k_verify_sig(StepParams P) {
         for (int i = 0; i < kDecAhead; ++i)
             if (i < nsteps) dec_issue(P, (c + i * grid) / NT, pre[i]);
     }
+    // One CTA barrier per tile: it publishes the tile's decision (double-
+    // buffered, so thread 0 may run one tile ahead) and proves every warp is
+    // done with the slot tile k - 1 used, which thread 0 then refills.
+    __shared__ Decision sdec[2];
     int slot_k = 0, slot_i = (nbuf - 1) % nbuf;
     for (int k = 0; k < nsteps; ++k) {
-        if (tid == 0 && spec && k + nbuf - 1 < nsteps) {
-            const int u = c + (k + nbuf - 1) * grid, b = u / NT;
-            sig_issue<T>(P, b, u - b * NT, bufp(slot_i), &bars[slot_i]);
-        }
         const int u = c + k * grid, b = u / NT, j = u - b * NT;
         if (tid == 0) {
             Decision d;
             if (!dec_decode(pre[0], d)) d = wait_decision(P, b);
-            sh.dec = d;
+            sdec[k & 1] = d;
 #pragma unroll
             for (int i = 0; i + 1 < kDecAhead; ++i) pre[i] = pre[i + 1];
             if (k + kDecAhead < nsteps) dec_issue(P, (u + kDecAhead * grid) / NT, pre[kDecAhead - 1]);
         }
-        __syncthreads();  // decision in sh.dec
-        const Decision d = sh.dec;
+        __syncthreads();  // decision of tile k published; tile k - 1's slot is free
+        if (tid == 0 && spec && k + nbuf - 1 < nsteps) {
+            const int ui = c + (k + nbuf - 1) * grid, bi = ui / NT;
+            sig_issue<T>(P, bi, ui - bi * NT, bufp(slot_i), &bars[slot_i]);
+        }
+        const Decision d = sdec[k & 1];
         if (spec) mbar_wait(&bars[slot_k], (uint32_t)((k / nbuf) & 1));  // tile k has landed
         const T* tb = reinterpret_cast<const T*>(bufp(slot_k));
         const int shift = (int)((reinterpret_cast<uintptr_t>(p_row<T>(P, b, P.G) + (size_t)j * TE) & 15) / sizeof(T));
@@ -1796,10 +1800,10 @@ __global__ void __launch_bounds__(kCtaThreads, 2) k_verify_sig(StepParams P) {
             }
         }
         if (j == 0 && tid == 0) trace(P, 8 * b + 3);
-        __syncthreads();  // buffer of step k is free
         slot_k = slot_k + 1 == nbuf ? 0 : slot_k + 1;
         slot_i = slot_i + 1 == nbuf ? 0 : slot_i + 1;
     }
+    __syncthreads();  // every warp's tiles are done
     // 3. inverse CDFs once every tile is in (a locate inside the stream stalls
     // its CTA for ~4 us of dependent round trips, and a locate waiting on a CTA
     // busy with its own chains the stalls: measured slower either way).
@@ -2947,15 +2951,16 @@ static void launch_slab_t(const StepParams& P, const Launch& L) {
 }
 
 // Sigmoid-stream geometry (sg_on 0 = not applicable): tiles of TE elements
-// (32 KB of one row), a ring of nbuf tiles per CTA, one CTA per SM.
+// (48 KB of one row), a ring of nbuf tiles per CTA, two CTAs per SM.
 template <typename T, int ACT>
 static bool plan_sig_t(StepParams& P) {
     P.sg_on = 0;
     if (P.sample_mode) return false;
-    const int TE = 32768 / (int)sizeof(T);  // multiple of kGW * kWarps
+    static const int te_kb = knob("SSV_SIG_TE_KB", 48);  // 48 KB tiles: 32 KB 55 us, 64 KB (one CTA per SM) 67 us at C4
+    const int TE = te_kb * 1024 / (int)sizeof(T) / (kGW * kWarps) * (kGW * kWarps);  // multiple of kGW * kWarps
     const int tb = ((TE + 2 * (16 / (int)sizeof(T))) * (int)sizeof(T) + 127) & ~127;
     // Two CTAs per SM (16 warps to hide the per-element MUFU chains), each a
-    // ring of two 32 KB tiles (three measured no faster) plus the locate's
+    // ring of two 48 KB tiles (three measured no faster) plus the locate's
     // granule cache.
     static const int nb_env = knob("SSV_SIG_NBUF", 0);
     const int nbuf = nb_env > 1 ? nb_env : 2;
