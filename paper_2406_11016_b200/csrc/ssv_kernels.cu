@@ -1811,6 +1811,159 @@ __global__ void __launch_bounds__(kCtaThreads, 2) k_verify_sig(StepParams P) {
     if (P.trace && tid == 0) atomicMax(&P.trace[8 * P.B + 1], gtime());
 }
 
+// K2w k_verify_sigw<T>: the sigmoid-stream kernel for 16-byte-aligned rows
+// (every row start and V * sizeof(T) a multiple of 16 -- C4), with no CTA
+// barrier in the stream: every warp owns whole units of the bonus row (256
+// 16-byte vectors = 2 fp32 / 4 bf16 granules), every thread cp.asyncs and later
+// reads only its own vectors through a kSigWStages-deep ring (the A-item
+// scheme), and lane 0 of each warp polls the decisions of its
+// next units.  Decisions first and the inverse CDFs last, as k_verify_sig.
+constexpr int kSigWNJ = 8;      // vectors per lane per unit
+constexpr int kSigWStages = 3;  // ring depth (2 units in flight per warp)
+constexpr int kSigWUnitVec = 32 * kSigWNJ;
+
+template <typename T, int ACT>
+__global__ void __launch_bounds__(kCtaThreads, 2) k_verify_sigw(StepParams P) {
+    __shared__ Shared sh;
+    extern __shared__ __align__(128) uint8_t sigw_smem[];
+    constexpr int VEC = Elem<T>::VEC;
+    constexpr int EU = kSigWUnitVec * VEC;  // elements per unit (1024 fp32, 2048 bf16)
+    constexpr int GU = EU / kGW;            // granules per unit (2, 4)
+    constexpr int JPG = kSigWNJ / GU;       // lane vectors per granule (4, 2)
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    pdl_enter();
+    const int grid = gridDim.x, c = blockIdx.x;
+    const int NTW = (P.V + EU - 1) / EU;   // units per row
+    const int NU = P.B * NTW;
+    const int nwarps = grid * kWarps, gw = c * kWarps + warp;
+    // Each warp takes a contiguous range of units (one or two rows): the
+    // decision changes only at a row boundary, and no division per unit.
+    const int u0 = (int)((long)gw * NU / nwarps), u1 = (int)((long)(gw + 1) * NU / nwarps);
+    const int nsteps = u1 - u0;
+    const int nvec_row = (P.V + VEC - 1) / VEC;
+    uint4* ring = reinterpret_cast<uint4*>(sigw_smem);  // [stage][j][thread]
+    double2* gcache = reinterpret_cast<double2*>(sigw_smem + (size_t)kSigWStages * kSigWNJ * kCtaThreads * 16);
+    if (P.trace && c == 0 && tid == 0) trace(P, 8 * P.B);
+    const bool spec = P.PS == P.G + 1;  // a bonus row exists: stream it speculatively
+    int ib = u0 / NTW, ij = u0 - ib * NTW;  // unit of the next issue
+    auto issue = [&](int stage) {
+        if (spec && ib < P.B && ib * NTW + ij < u1) {
+            const uint4* rowv = reinterpret_cast<const uint4*>(p_row<T>(P, ib, P.G)) + ij * kSigWUnitVec + lane;
+            uint4* dst = ring + (size_t)stage * kSigWNJ * kCtaThreads + tid;
+            const int nv = nvec_row - ij * kSigWUnitVec - lane;  // vectors left in the row from this lane's first
+#pragma unroll
+            for (int j = 0; j < kSigWNJ; ++j)
+                if (j * 32 < nv) cp_async16(dst + j * kCtaThreads, rowv + j * 32);
+        }
+        cp_async_commit();
+        if (++ij == NTW) {
+            ij = 0;
+            ++ib;
+        }
+    };
+    // 1. decisions from the gathers: row b on warp (b / grid) % 8 of CTA b % grid,
+    // so most CTAs lose one warp for ~4 us instead of a few CTAs all eight
+    for (int b = c + grid * warp; b < P.B; b += grid * kWarps) {
+        Decision d;
+        decide_gather<T, ACT>(P, b, true, d);
+        __syncwarp();
+        if (lane == 0) {
+            publish_decision(P, b, d);
+            trace(P, 8 * b + 2);
+        }
+    }
+    for (int k = 0; k < kSigWStages - 1; ++k) issue(k);
+    int b = u0 / NTW, jw = u0 - b * NTW;
+    DecRaw pre;
+    if (lane == 0 && nsteps > 0) dec_issue(P, b, pre);
+    int mode = 0, row = 0;
+    const float sc = (float)(-1.4426950408889634 / P.width);
+    const float off = (float)(P.alpha * 1.4426950408889634 / P.width);
+    int stage = 0;
+    for (int k = 0; k < nsteps; ++k) {
+        issue((stage + kSigWStages - 1) % kSigWStages);
+        if (k == 0 || jw == 0) {  // a new row: its decision (the next row's words go in flight)
+            if (lane == 0) {
+                Decision dd;
+                if (!dec_decode(pre, dd)) dd = wait_decision(P, b);
+                mode = dd.mode;
+                row = dd.row;
+                if (b + 1 < P.B && (b + 1) * NTW < u1) dec_issue(P, b + 1, pre);
+            }
+            mode = __shfl_sync(kFull, mode, 0);
+            row = __shfl_sync(kFull, row, 0);
+        }
+        cp_async_wait<kSigWStages - 1>();  // this thread's vectors of unit k have landed
+        const int g0 = jw * GU;
+        double2* out = P.gpart + (size_t)b * P.NG;
+        if (mode == MODE_BONUS) {
+            const int nv = nvec_row - jw * kSigWUnitVec - lane;
+            const uint4* src = ring + (size_t)stage * kSigWNJ * kCtaThreads + tid;
+            double acc[GU];
+#pragma unroll
+            for (int h = 0; h < GU; ++h) {
+                float a = 0.f;
+#pragma unroll
+                for (int jj = 0; jj < JPG; ++jj) {
+                    const int j = h * JPG + jj;
+                    if (j * 32 < nv) {  // (rows are whole vectors: no element mask)
+                        float x[VEC];
+                        unpack(src[j * kCtaThreads], x);
+#pragma unroll
+                        for (int e = 0; e < VEC; ++e) {
+                            const float ex = ex2f(fmaf(x[e], sc, off));
+                            float r;
+                            asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(1.0f + ex));
+                            a += r;
+                        }
+                    }
+                }
+                acc[h] = a;
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+                for (int h = 0; h < GU; ++h) acc[h] += __shfl_xor_sync(kFull, acc[h], o);
+            if (lane == 0) {
+#pragma unroll
+                for (int h = 0; h < GU; ++h)
+                    if (g0 + h < P.NG) st_slot(&out[g0 + h], make_double2(0.0, acc[h]));
+            }
+        } else {
+            Decision d{};
+            d.mode = mode;
+            d.row = row;
+            d.Sp = d.Sq = 1.0;
+            // (rare at the sigmoid's acceptance) the pair from global, two
+            // granules' loads in flight at a time
+            for (int h = 0; h < GU; h += 2) {
+                GranuleData<T> D[2];
+#pragma unroll
+                for (int q = 0; q < 2; ++q)
+                    if (mode == MODE_REJECT && g0 + h + q < P.NG) granule_load<T>(P, b, g0 + h + q, d, D[q]);
+#pragma unroll
+                for (int q = 0; q < 2; ++q) {
+                    if (g0 + h + q >= P.NG) break;
+                    double2 gv = make_double2(0.0, 0.0);
+                    if (mode == MODE_REJECT) gv = granule_reduce<T, ACT>(P, d, D[q]);
+                    if (lane == 0) st_slot(&out[g0 + h + q], gv);
+                }
+            }
+        }
+        if (jw == 0 && lane == 0) trace(P, 8 * b + 3);
+        stage = stage + 1 == kSigWStages ? 0 : stage + 1;
+        if (++jw == NTW) {
+            jw = 0;
+            ++b;
+        }
+    }
+    cp_async_wait<0>();
+    if (P.trace && P.sl_dbg && lane == 0) P.trace[8 * P.B + 26 + gw] = gtime();  // experiment: warp loop end
+    __syncthreads();
+    for (int b = grid - 1 - c; b < P.B; b += grid) locate_row<T, ACT>(P, b, sh, gcache);
+    if (P.trace && tid == 0) atomicMax(&P.trace[8 * P.B + 1], gtime());
+}
+
 // ---------------------------------------------------------------------------
 // K1c/K2c k_verify_cluster<T, ACT>: the cluster path.  One
 // thread-block cluster of cl_size (16 down to 4) CTAs per batch row; rank k
@@ -2975,6 +3128,31 @@ static bool plan_sig_t(StepParams& P) {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_verify_sig<T, ACT>, kCtaThreads, smem);
     if (per_sm < 1) return false;
     P.sg_on = 1;
+    P.sg_warp = 0;
+    static const int sl_dbg = knob("SSV_SLAB_TRACE", 0);
+    P.sl_dbg = sl_dbg;
+    {  // 16-byte-aligned rows: the barrier-free warp kernel
+        const bool aligned = (reinterpret_cast<uintptr_t>(P.zp) & 15) == 0 && ((size_t)P.V * sizeof(T)) % 16 == 0;
+        static const int no_warp = knob("SSV_SIG_NO_WARP", 0);
+        if (aligned && !no_warp) {
+            const int smemw = kSigWStages * kSigWNJ * kCtaThreads * 16 + std::min(P.NG, kLocCap) * (int)sizeof(double2);
+            static bool attrw = false;
+            if (!attrw) {
+                cudaFuncSetAttribute(k_verify_sigw<T, ACT>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSlabSmemMax);
+                attrw = true;
+            }
+            int pw = 0;
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pw, k_verify_sigw<T, ACT>, kCtaThreads, smemw);
+            if (pw >= 1) {
+                P.sg_warp = 1;
+                P.sg_smem = smemw;
+                P.sg_grid = sm_count() * pw;
+                P.sg_te = TE;
+                P.sg_nt = (P.V + TE - 1) / TE;
+                return true;
+            }
+        }
+    }
     P.sg_te = TE;
     P.sg_nt = (P.V + TE - 1) / TE;
     P.sg_nbuf = nbuf;
@@ -3005,7 +3183,8 @@ static void launch_sig_t(const StepParams& P, const Launch& L) {
     cfg.attrs = at;
     cfg.numAttrs = 1 + pdl_attr(at[1]);
     const int h = L.begin(KID_VERIFY);
-    cudaLaunchKernelEx(&cfg, k_verify_sig<T, ACT>, P);
+    if (P.sg_warp) cudaLaunchKernelEx(&cfg, k_verify_sigw<T, ACT>, P);
+    else cudaLaunchKernelEx(&cfg, k_verify_sig<T, ACT>, P);
     L.end(h);
 }
 

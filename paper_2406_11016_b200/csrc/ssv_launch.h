@@ -87,6 +87,7 @@ struct StepParams {
     // elements of each batch row's needed row, sg_nt per row, a ring of sg_nbuf
     // tile buffers of sg_tb bytes per CTA.
     int sg_on, sg_te, sg_nt, sg_nbuf, sg_tb, sg_smem, sg_grid;
+    int sg_warp;  // 1: k_verify_sigw (16-byte-aligned rows, barrier-free warp units)
     int dbg;  // experiment bits (SSV_DBG_MODE), 0 in production
     double alpha, width;
     int sample_mode;     // sample softmax(z_p row b) with u[b] (draft sampling)

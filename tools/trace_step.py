@@ -25,7 +25,7 @@ run = (lambda: v.verify_exact(zp, zq, ids, u)) if a.variant == "exact" else (lam
 for _ in range(3):
     run()
 torch.cuda.synchronize()
-cap = 8 * a.B + 26 + 148 * 8
+cap = 8 * a.B + 26 + 296 * 8
 v.trace_enable(cap)
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 s = torch.cuda.Stream()
@@ -48,6 +48,10 @@ rows = list(range(min(a.B, 16))) + (list(range(16, a.B, max(1, a.B // 16))) if a
 for b in rows:
     p = ph[b]
     print(f"b={b:3d} {acc[b]} | D {f(p[0])} {f(p[1])} {f(p[2])} | B {f(p[3])} {f(p[4])} | L {f(p[5])} {f(p[6])} {f(p[7])}")
+lend = ph[:, 7].astype(np.int64)
+if (lend > 0).any():
+    worst = np.argsort(-lend)[:5]
+    print("latest row ends (us):", ", ".join(f"b={w} {(lend[w] - t0) / 1e3:.1f}" for w in worst))
 ex = t[8 * a.B + 2: 8 * a.B + 18]
 if ex[0] > 0:
     print("row-0 fine stamps (us):", " ".join(f"{(x - t0) / 1e3:.1f}" if x > 0 else "-" for x in ex))
@@ -68,3 +72,11 @@ if os.environ.get("SSV_SLAB_TRACE"):
         col = ct[:, k][ct[:, k] > 0]
         if len(col):
             print(f"step {k}: stats done min {(col.min() - t0) / 1e3:.1f} max {(col.max() - t0) / 1e3:.1f} us")
+
+if os.environ.get("SSV_SIG_TRACE"):
+    we = t[8 * a.B + 26: 8 * a.B + 26 + 296 * 8].astype(np.int64)
+    ok = we > 0
+    rel = (we[ok] - t0) / 1e3
+    print(f"warp loop ends: n={ok.sum()} min {rel.min():.1f} median {np.median(rel):.1f} max {rel.max():.1f} us")
+    worst = np.argsort(-np.where(ok, we, 0))[:8]
+    print("latest warps:", ", ".join(f"gw={w} {(we[w] - t0) / 1e3:.1f}" for w in worst))
