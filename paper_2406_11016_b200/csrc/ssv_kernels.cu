@@ -2371,7 +2371,42 @@ __global__ void __launch_bounds__(NT, 1) k_verify_cluster(StepParams P) {
     if (tr) trace(P, 8 * b + 4);
     cl.sync();  // rank totals delivered; granule masses visible in global memory
     if (tr) trace(P, 8 * b + 5);
-    if (d.mode == MODE_NONE) return;
+    // Optional p / q / residual grids straight from the resident slices (no
+    // second pass over the logits): every rank writes its slice of every row
+    // -- the locator after its scan, the others instead of exiting early.
+    auto write_grids = [&]() {
+        if constexpr (EXACT) {
+            if (!P.fuse_grids || n <= 0) return;
+            float* gp = reinterpret_cast<float*>(P.grid_p);
+            float* gq = reinterpret_cast<float*>(P.grid_q);
+            float* gr = reinterpret_cast<float*>(P.grid_r);
+            for (int c = 0; c <= G; ++c) {
+                const bool pair = c < G;
+                if (!pair && (!gp || NRc <= 2 * G)) break;
+                const int rp = pair ? c : 2 * G;
+                const T* xp = reinterpret_cast<const T*>(slots + (size_t)rp * RB) + offs[rp];
+                const T* xq = pair ? reinterpret_cast<const T*>(slots + (size_t)(G + c) * RB) + offs[G + c] : xp;
+                const float Mp = (float)sh.rs[rp].x, iSp = (float)(1.0 / sh.rs[rp].y);
+                const float Mq = pair ? (float)sh.rs[G + c].x : 0.f, iSq = pair ? (float)(1.0 / sh.rs[G + c].y) : 0.f;
+                float* op = gp ? gp + ((size_t)b * P.PS + c) * (size_t)V + e0 : nullptr;
+                float* oq = gq && pair ? gq + ((size_t)b * G + c) * (size_t)V + e0 : nullptr;
+                float* orr = gr && pair ? gr + ((size_t)b * G + c) * (size_t)V + e0 : nullptr;
+                for (int i = tid; i < n; i += NT) {
+                    const float pv = exp_rel_acc(load_smem_elem(xp + i), Mp) * iSp;
+                    if (op) op[i] = pv;
+                    if (oq || orr) {
+                        const float qv = exp_rel_acc(load_smem_elem(xq + i), Mq) * iSq;
+                        if (oq) oq[i] = qv;
+                        if (orr) orr[i] = pv - qv > 0.f ? pv - qv : 0.f;
+                    }
+                }
+            }
+        }
+    };
+    if (d.mode == MODE_NONE) {
+        write_grids();
+        return;
+    }
     const double u = zg[2 * G + G];  // u_final (verify_reference.cpp:98)
     // Every rank combines the totals in the same order: denominators
     // (verify_reference.cpp:51-62 / dist.cpp:114-121 at slice resolution) and
@@ -2415,7 +2450,10 @@ __global__ void __launch_bounds__(NT, 1) k_verify_cluster(StepParams P) {
     }
     __syncthreads();
     const int owner = sh.loc_g;
-    if (rank != (owner >= 0 ? owner : 0)) return;  // one locator per batch row
+    if (rank != (owner >= 0 ? owner : 0)) {  // one locator per batch row
+        write_grids();
+        return;
+    }
     const bool tl = P.trace && b == 0 && tid == 0;  // locate stamps: trace[8B + 18 ..]
     if (tr) trace(P, 8 * b + 6);
     if (tl) trace(P, 8 * P.B + 21);
@@ -2501,6 +2539,7 @@ __global__ void __launch_bounds__(NT, 1) k_verify_cluster(StepParams P) {
             atomicMax(&P.trace[8 * P.B + 1], gtime());
         }
     }
+    write_grids();
 }
 
 // ---------------------------------------------------------------------------
@@ -3210,20 +3249,31 @@ static void launch_step_t(const StepParams& P, const Launch& L) {
 }
 
 template <typename T>
-static void dispatch_verify(int act, const StepParams& P, void* outp, void* outq, void* outr, const Launch& L) {
+static void dispatch_verify(int act, const StepParams& P0, void* outp, void* outq, void* outr, const Launch& L) {
     const bool mat = outp || outq || outr;
     if (act == ACT_SOFTMAX) {
+        // Resident cluster plan: the verify kernel writes the grids from the
+        // slices it still holds; otherwise k_materialize is a second pass.
+        StepParams P = P0;
+        static const bool no_fuse = knob_set("SSV_NO_FUSE_GRIDS");
+        const bool fuse = mat && sizeof(T) != 8 && P.cl_size > 0 && P.cl_resident && !no_fuse;
+        if (fuse) {
+            P.fuse_grids = 1;
+            P.grid_p = outp;
+            P.grid_q = outq;
+            P.grid_r = outr;
+        }
         launch_step_t<T, ACT_SOFTMAX>(P, L);
-        if (mat) launch_mat_t<T, ACT_SOFTMAX>(P, outp, outq, outr, L);
+        if (mat && !fuse) launch_mat_t<T, ACT_SOFTMAX>(P, outp, outq, outr, L);
     } else if (act == ACT_SIGMOID) {
-        launch_step_t<T, ACT_SIGMOID>(P, L);
-        if (mat) launch_mat_t<T, ACT_SIGMOID>(P, outp, outq, outr, L);
+        launch_step_t<T, ACT_SIGMOID>(P0, L);
+        if (mat) launch_mat_t<T, ACT_SIGMOID>(P0, outp, outq, outr, L);
     } else if (act == ACT_SIGMOID_HALF) {
-        launch_step_t<T, ACT_SIGMOID_HALF>(P, L);
-        if (mat) launch_mat_t<T, ACT_SIGMOID_HALF>(P, outp, outq, outr, L);
+        launch_step_t<T, ACT_SIGMOID_HALF>(P0, L);
+        if (mat) launch_mat_t<T, ACT_SIGMOID_HALF>(P0, outp, outq, outr, L);
     } else {
-        launch_step_t<T, ACT_PROBS>(P, L);
-        if (mat) launch_mat_t<T, ACT_PROBS>(P, outp, outq, outr, L);
+        launch_step_t<T, ACT_PROBS>(P0, L);
+        if (mat) launch_mat_t<T, ACT_PROBS>(P0, outp, outq, outr, L);
     }
 }
 

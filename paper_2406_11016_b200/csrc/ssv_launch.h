@@ -88,6 +88,13 @@ struct StepParams {
     // tile buffers of sg_tb bytes per CTA.
     int sg_on, sg_te, sg_nt, sg_nbuf, sg_tb, sg_smem, sg_grid;
     int sg_warp;  // 1: k_verify_sigw (16-byte-aligned rows, barrier-free warp units)
+    // Optional grids written by the verify kernel itself (resident cluster plan:
+    // every row slice is still in shared memory after the decision), else by
+    // k_materialize as a second pass.
+    int fuse_grids;
+    void* grid_p;
+    void* grid_q;
+    void* grid_r;
     int dbg;  // experiment bits (SSV_DBG_MODE), 0 in production
     double alpha, width;
     int sample_mode;     // sample softmax(z_p row b) with u[b] (draft sampling)
