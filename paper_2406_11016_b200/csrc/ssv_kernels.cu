@@ -1,36 +1,43 @@
 // ssv_kernels.cu -- sm_100a kernels of the speculative-sampling verification step.
 //
-// Two single-launch implementations of the whole step (DESIGN.md 3 has the
-// derivation and the roofline); the host picks one per call (plan_cluster):
+// Single-launch implementations of the whole step (DESIGN.md 3 has the
+// derivation and the roofline); the host picks one per call (plan_cluster,
+// plan_sig, plan_slab):
 //
-// k_verify<T, ACT> -- streaming path (any size; C4).  Persistent 256-thread
-// CTAs claim work items in order from a global counter; every wait is on an
-// item with a smaller claim index (held by a running CTA), so any grid size is
-// deadlock-free.  Items of batch row b:
+// k_verify<T, ACT> -- streaming path (any size; C4 exact).  Persistent
+// 256-thread CTAs claim work items in order from a global counter; every wait
+// is on an item with a smaller claim index (held by a running CTA), so any
+// grid size is deadlock-free.  Items of batch row b:
 //   A-item  (exact only) a run of 32 KB chunks of one drafted p / q row through
 //           a 2-deep cp.async ring of per-thread 16-byte slots (no barrier);
 //           per thread a running max (FMNMX3 / packed bf16 max) and
 //           sum e^(x - max) (FADD2/FMUL2 + MUFU ex2 in fp32 pairs of <= 16
-//           terms, fp64 across); one fp64 partial per warp.  The next claimed
-//           run's first chunk streams while this run drains.
-//   D-item  exact: folds b's partials into row statistics, tau at every
+//           terms, fp64 across); one fp64 partial per warp, stored into its
+//           self-flagging slot (no release fence).  The next claimed run's
+//           first chunk streams while this run drains.
+//   D-item  exact: folds b's partial slots into row statistics, tau at every
 //           drafted position in fp64 (activation.cpp:20-27 +
 //           verify_reference.cpp:87-92), first rejection (93-96); sigmoid /
 //           probabilities: the decision from the B*gamma gathered values alone
-//           (paper section 3.2.2).  Publishes the decision (release flag).
+//           (paper section 3.2.2).  Publishes the decision slots.
 //   B-item  8192 elements of the ONE row (bonus) or row PAIR (rejected
-//           position) b still needs -> 512-element granule masses (L2-hot
-//           re-read of the rejected pair).
+//           position) b still needs -> 512-element granule masses (re-read of
+//           the rejected pair) into the granule slots.
 //   L-item  inverse CDF: fp64 granule prefix, then the exact fp64 element scan
-//           (locate_scan; dist.cpp:122-137 incl. its fallbacks); resets b's
-//           counters.
+//           (locate_scan; dist.cpp:122-137 incl. its fallbacks); clears b's
+//           slots.
 //
 // k_verify_cluster<T, ACT> -- cluster path (batches whose rows each get a
 // co-resident thread-block cluster; C1-C3), described above the kernel.
+// k_verify_sigw / k_verify_sig<T> -- the sigmoid variant beyond the cluster
+// path (C4 sigmoid): decisions from the gathers first, then the bonus rows
+// streamed once (barrier-free warp units for aligned rows, TMA tiles else).
+// k_verify_slab<T> -- experimental exact kernel keeping every drafted row
+// slice in shared memory until its decision (SSV_PATH_SLAB only).
 //
 // Every reduction has a fixed topology, so results are bit-identical run to
-// run.  k_materialize (optional p / q / residual grids) and the synthetic-input
-// generator follow.
+// run.  k_materialize (optional p / q / residual grids when the verify kernel
+// does not write them itself) and the synthetic-input generator follow.
 #include <algorithm>
 #include <cfloat>
 #include <cstdio>
