@@ -25,6 +25,8 @@ SSV_OK, SSV_ECUDA, SSV_EINVAL = 0, 1, 2
 SSV_F32, SSV_BF16, SSV_F64 = 0, 1, 2
 SSV_WANT_P, SSV_WANT_Q, SSV_WANT_RESIDUAL = 1, 2, 4
 SSV_EMULATE_HALF = 8
+# device status bits (ssv.h SSV_STATUS_*)
+SSV_STATUS_NONFINITE, SSV_STATUS_TOKEN_RANGE, SSV_STATUS_UNIFORM_RANGE, SSV_STATUS_NEGATIVE = 1, 2, 4, 8
 
 
 class SsvError(RuntimeError):

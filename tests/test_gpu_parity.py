@@ -546,3 +546,42 @@ def test_locate_edges_exact_logits(verifier, oracle, path):
         assert compare(ob, gb, zpb, zqb, ids, u, "exact", label=f"{path}-bf16-locate") == 0
     finally:
         verifier.set_path("auto")
+
+
+@pytest.mark.parametrize("path", ["streaming", "cluster", "cluster_ring", "slab"])
+def test_nonfinite_blocks_every_plan(verifier, oracle, path):
+    """require_finite (dist.cpp:27-36) on whole blocks, not just one element:
+    a 4096-element NaN block at the start of a row (a whole streaming chunk /
+    cluster slice of NaN), a row of -inf, and a single +inf -- every plan sets
+    the non-finite status bit (the reference throws)."""
+    import torch
+
+    from paper_2406_11016_b200.ssv import SSV_STATUS_NONFINITE
+
+    rng = np.random.default_rng(5)
+    B, gamma, V = 2, 3, 51865
+    zq = oracle.round_f32(rng.normal(0.0, 2.0, (B, gamma, V)))
+    zp = oracle.round_f32(np.concatenate([zq + rng.normal(0.0, 0.5, (B, gamma, V)), rng.normal(0.0, 2.0, (B, 1, V))],
+                                         axis=1))
+    ids = rng.integers(0, V, (B, gamma)).astype(np.int32)
+    u = rng.random((B, gamma + 1))
+    cases = []
+    a = zq.copy()
+    a[1, 2, :4096] = np.nan
+    cases.append(("nan-block", zp, a))
+    a = zp.copy()
+    a[0, 1, :] = -np.inf
+    cases.append(("row-of-minus-inf", a, zq))
+    a = zq.copy()
+    a[0, 0, V - 1] = np.inf
+    cases.append(("plus-inf", zp, a))
+    verifier.set_path(path)
+    try:
+        for name, p_, q_ in cases:
+            t = to_device(oracle, p_, q_, ids, u, "f32")
+            r = verifier.verify_exact(*t)
+            torch.cuda.synchronize()
+            st = int(r.status.item())
+            assert st & SSV_STATUS_NONFINITE, f"{path} {name}: status {st}"
+    finally:
+        verifier.set_path("auto")
