@@ -1060,20 +1060,16 @@ __device__ void locate(const StepParams& P, int b, const Decision& d, Shared& sh
     auto raw = [&](int g) -> double2 { return g < kLocCap ? gcache[g] : __ldcg(&gp[g]); };
 
     // Level 1 on warp 0 alone (no block barriers): the denominators, then the
-    // fp64 granule prefix over contiguous lane ranges (verify_reference.cpp:
-    // 51-62 / dist.cpp:122-137 at granule resolution); lane 0 publishes.
+    // fp64 granule prefix (verify_reference.cpp:51-62 / dist.cpp:122-137 at
+    // granule resolution); lane 0 publishes.  Lane l takes granules l, l + 32,
+    // ... (conflict-free shared-memory reads; a lane-contiguous layout made
+    // every read an 8-way bank conflict and the search a serial chain: ~4700
+    // cycles at NG = 297), one warp scan per 32-granule round in the search.
     if (threadIdx.x < 32) {
         const int lane = threadIdx.x;
-        const int gpl = (NG + 31) / 32;
-        const int ga = min(NG, lane * gpl), gb = min(NG, ga + gpl);
+        const int rounds = (NG + 31) / 32;
         bool useA = false;
         double denom = 1.0, gM = 0.0, gS = 1.0;
-        // One pass over the lane's granules and ONE warp scan of unnormalized
-        // masses give both the denominators (the scan totals) and each lane's
-        // prefix; the search then compares against u * denominator (the exact
-        // per-term division happens in level 2).  Short dependency chain: this
-        // runs on one warp between two barriers.
-        double run = 0.0, thr = 0.0;
         auto wraw = [&](int g) -> double {  // unnormalized granule mass
             const double2 v = raw(g);
             if (d.mode == MODE_REJECT) return useA ? v.x : v.y;
@@ -1082,17 +1078,15 @@ __device__ void locate(const StepParams& P, int b, const Decision& d, Shared& sh
         };
         if (d.mode == MODE_REJECT) {
             double a1 = 0.0, a2 = 0.0;
-            for (int g = ga; g < gb; ++g) {
+            for (int g = lane; g < NG; g += 32) {
                 const double2 v = raw(g);
                 a1 += v.x;
                 a2 += v.y;
             }
             if (P.trace && b == 0 && lane == 0) P.trace[8 * P.B + 23] = (unsigned long long)(clock64() - cyc0);
-            const double i1 = warp_scan_incl(a1), i2 = warp_scan_incl(a2);
-            const double sa = __shfl_sync(kFull, i1, 31), sp = __shfl_sync(kFull, i2, 31);
+            const double sa = warp_sum(a1), sp = warp_sum(a2);
             useA = sa > kZeroEps;  // verify_reference.cpp:57-62
             denom = useA ? sa : sp;
-            run = useA ? i1 - a1 : i2 - a2;
             if (lane == 0) {
                 if (P.rsu) P.rsu[b] = 1;
                 if (P.rden) P.rden[b] = useA ? sa : 0.0;
@@ -1101,9 +1095,9 @@ __device__ void locate(const StepParams& P, int b, const Decision& d, Shared& sh
             double sm = 0.0;
             if (ACT == ACT_SOFTMAX) {  // the bonus row's statistics from its granules
                 double m = -CUDART_INF;
-                for (int g = ga; g < gb; ++g) m = fmax(m, raw(g).x);
+                for (int g = lane; g < NG; g += 32) m = fmax(m, raw(g).x);
                 gM = warp_max(m);
-                for (int g = ga; g < gb; ++g) {
+                for (int g = lane; g < NG; g += 32) {
                     const double2 v = raw(g);
                     const double w = v.y > 0.0 ? v.y * exp(v.x - gM) : 0.0;
                     sm += w;
@@ -1111,14 +1105,13 @@ __device__ void locate(const StepParams& P, int b, const Decision& d, Shared& sh
                     // mass, and the search below needs no further exp
                     if (g < kLocCap) gcache[g] = make_double2(gM, w);
                 }
+                __syncwarp();
             } else {
-                for (int g = ga; g < gb; ++g) sm += raw(g).y;
+                for (int g = lane; g < NG; g += 32) sm += raw(g).y;
             }
-            const double incl = warp_scan_incl(sm);
-            const double tot = __shfl_sync(kFull, incl, 31);
+            const double tot = warp_sum(sm);
             if (ACT == ACT_SOFTMAX) gS = tot;
             else denom = tot;
-            run = incl - sm;
             if (lane == 0) {
                 if (P.rsu) P.rsu[b] = 0;
                 if (P.rden) P.rden[b] = 0.0;
@@ -1126,22 +1119,23 @@ __device__ void locate(const StepParams& P, int b, const Decision& d, Shared& sh
         }
         if (P.trace && b == 0 && lane == 0) P.trace[8 * P.B + 24] = (unsigned long long)(clock64() - cyc0);
         const double norm = d.mode != MODE_REJECT && ACT == ACT_SOFTMAX ? gS : denom;
-        thr = u * norm;
-        int hit = 0x7fffffff;
-        double hit_carry = 0.0;
-        for (int g = ga; g < gb; ++g) {
-            const double w = wraw(g);
-            if (thr < run + w) {
-                hit = g;
-                hit_carry = run / norm;
+        const double thr = u * norm;
+        int gst = -1;
+        double car = 0.0, carry = 0.0;
+        for (int j = 0; j < rounds; ++j) {  // first granule whose inclusive prefix passes u * norm
+            const int g = lane + 32 * j;
+            const double w = g < NG ? wraw(g) : 0.0;
+            const double incl = warp_scan_incl(w);
+            const unsigned hm = __ballot_sync(kFull, g < NG && thr < carry + incl);
+            if (hm) {
+                const int src = __ffs(hm) - 1;
+                gst = 32 * j + src;
+                car = (carry + __shfl_sync(kFull, incl - w, src)) / norm;
                 break;
             }
-            run += w;
+            carry += __shfl_sync(kFull, incl, 31);
         }
-        const unsigned hm = __ballot_sync(kFull, hit != 0x7fffffff);
-        const int src = hm ? __ffs(hm) - 1 : 0;
-        const int gst = __shfl_sync(kFull, hit, src);
-        const double car = __shfl_sync(kFull, hit_carry, src);
+        const unsigned hm = gst >= 0 ? 1u : 0u;
         if (lane == 0) {
             if (P.trace && b == 0) {
                 P.trace[8 * P.B + 22] = (unsigned long long)(clock64() - cyc0);
