@@ -952,6 +952,25 @@ __device__ __forceinline__ double2 granule_reduce(const StepParams& P, const Dec
         return make_double2(warp_sum(ta), warp_sum(tp));
     }
     const A Mp = (A)d.Mp, Mq = (A)d.Mq, iSp = (A)(1.0 / d.Sp), iSq = (A)(1.0 / d.Sq);
+    if constexpr (ACT == ACT_SOFTMAX && sizeof(A) == 4) {
+        if (n == kGW) {  // full granule (warp-uniform): packed pairs, FADD2 / FMUL2 (the same roundings per term)
+            const float2 l2e = make_float2(1.4426950408889634f, 1.4426950408889634f);
+            const float2 nMp = make_float2(-Mp, -Mp), nMq = make_float2(-Mq, -Mq);
+            const float2 sP = make_float2(iSp, iSp), sQ = make_float2(iSq, iSq);
+            float2 ta2 = make_float2(0.f, 0.f), tp2 = make_float2(0.f, 0.f);  // 8 terms per chain
+#pragma unroll
+            for (int t = 0; t < EPL; t += 2) {
+                const float2 ap = __fmul2_rn(__fadd2_rn(make_float2(D.xs[t], D.xs[t + 1]), nMp), l2e);
+                const float2 aq = __fmul2_rn(__fadd2_rn(make_float2(D.xq[t], D.xq[t + 1]), nMq), l2e);
+                const float2 vp = __fmul2_rn(make_float2(ex2f(ap.x), ex2f(ap.y)), sP);
+                const float2 vq = __fmul2_rn(make_float2(ex2f(aq.x), ex2f(aq.y)), sQ);
+                const float2 dv = __fadd2_rn(vp, make_float2(-vq.x, -vq.y));
+                ta2 = __fadd2_rn(ta2, make_float2(dv.x > 0.f ? dv.x : 0.f, dv.y > 0.f ? dv.y : 0.f));
+                tp2 = __fadd2_rn(tp2, vp);
+            }
+            return make_double2(warp_sum((double)ta2.x + (double)ta2.y), warp_sum((double)tp2.x + (double)tp2.y));
+        }
+    }
     A ta = 0, tp = 0;
 #pragma unroll
     for (int t = 0; t < EPL; ++t) {
