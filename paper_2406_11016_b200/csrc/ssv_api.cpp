@@ -25,7 +25,7 @@ struct ssv_ctx {
     // stream-ordered scratch
     void* scratch = nullptr;
     size_t scratch_bytes = 0;
-    unsigned* counters = nullptr;  // [2]: next, exit (kernels leave them 0)
+    unsigned* counters = nullptr;  // [4]: next, exit, rejected rows, decisions (kernels leave them 0)
     void* slots = nullptr;  // streaming kernel's self-flagging slots (part, gpart): all kSlotEmpty between launches
     size_t slots_bytes = 0;
     uint32_t* status_dev = nullptr;  // default status word
@@ -129,9 +129,9 @@ int ensure_scratch(ssv_ctx* ctx, size_t bytes, size_t slot_bytes) {
         ctx->scratch_bytes = nb;
     }
     if (!ctx->counters) {
-        CK(cudaMalloc(&ctx->counters, 2 * sizeof(unsigned)));
+        CK(cudaMalloc(&ctx->counters, 4 * sizeof(unsigned)));
         // on the context's stream: the kernels that read the counters follow it
-        CK(cudaMemsetAsync(ctx->counters, 0, 2 * sizeof(unsigned), ctx->stream));
+        CK(cudaMemsetAsync(ctx->counters, 0, 4 * sizeof(unsigned), ctx->stream));
     }
     if (slot_bytes > ctx->slots_bytes) {
         if (ctx->slots) CK(cudaFree(ctx->slots));
@@ -146,7 +146,7 @@ int ensure_scratch(ssv_ctx* ctx, size_t bytes, size_t slot_bytes) {
 }
 
 struct Layout {
-    size_t rowstat, cgpart, extra, total;  // scratch
+    size_t rowstat, cgpart, rejl, extra, total;  // scratch
     size_t part, gpart, dslot, slots;      // slot region
 };
 
@@ -157,6 +157,8 @@ Layout plan_scratch(const StepParams& P, size_t extra_bytes) {
     off = align_up(off + (size_t)P.B * std::max(P.NR, 1) * sizeof(double2));
     L.cgpart = off;
     off = align_up(off + (size_t)P.B * P.NG * sizeof(double2));
+    L.rejl = off;
+    off = align_up(off + (size_t)P.B * sizeof(int));
     L.extra = off;
     off = align_up(off + extra_bytes);
     L.total = off;
@@ -181,6 +183,9 @@ void bind_scratch(ssv_ctx* ctx, StepParams& P, const Layout& L) {
     P.cgpart = reinterpret_cast<double2*>(s + L.cgpart);
     P.next = ctx->counters;
     P.exit_cnt = ctx->counters + 1;
+    P.rej_cnt = ctx->counters + 2;
+    P.dec_cnt = ctx->counters + 3;
+    P.rej_list = reinterpret_cast<int*>(s + L.rejl);
 }
 
 int run_device(ssv_ctx* ctx, int variant, const ssv_verify_args* a, ssv_verify_out* o) {

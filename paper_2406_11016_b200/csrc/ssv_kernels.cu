@@ -1866,8 +1866,11 @@ __global__ void __launch_bounds__(kCtaThreads, 2) k_verify_sigw(StepParams P) {
     if (P.trace && c == 0 && tid == 0) trace(P, 8 * P.B);
     const bool spec = P.PS == P.G + 1;  // a bonus row exists: stream it speculatively
     int ib = u0 / NTW, ij = u0 - ib * NTW;  // unit of the next issue
+    int cur_b = -1, cur_mode = MODE_NONE, cur_row = 0;  // the consumed row's decision, once known
     auto issue = [&](int stage) {
-        if (spec && ib < P.B && ib * NTW + ij < u1) {
+        if (ib == cur_b && cur_mode == MODE_REJECT) {
+            // a rejected row: no bonus tile (its pair is reduced in the reject phase)
+        } else if (spec && ib < P.B && ib * NTW + ij < u1) {
             const uint4* rowv = reinterpret_cast<const uint4*>(p_row<T>(P, ib, P.G)) + ij * kSigWUnitVec + lane;
             uint4* dst = ring + (size_t)stage * kSigWNJ * kCtaThreads + tid;
             const int nv = nvec_row - ij * kSigWUnitVec - lane;  // vectors left in the row from this lane's first
@@ -1889,6 +1892,9 @@ __global__ void __launch_bounds__(kCtaThreads, 2) k_verify_sigw(StepParams P) {
         __syncwarp();
         if (lane == 0) {
             publish_decision(P, b, d);
+            if (d.mode == MODE_REJECT) P.rej_list[atomicAdd(P.rej_cnt, 1u)] = b;
+            __threadfence();  // the list entry before the count
+            atomicAdd(P.dec_cnt, 1u);
             trace(P, 8 * b + 2);
         }
     }
@@ -1901,7 +1907,6 @@ __global__ void __launch_bounds__(kCtaThreads, 2) k_verify_sigw(StepParams P) {
     const float off = (float)(P.alpha * 1.4426950408889634 / P.width);
     int stage = 0;
     for (int k = 0; k < nsteps; ++k) {
-        issue((stage + kSigWStages - 1) % kSigWStages);
         if (k == 0 || jw == 0) {  // a new row: its decision (the next row's words go in flight)
             if (lane == 0) {
                 Decision dd;
@@ -1912,7 +1917,11 @@ __global__ void __launch_bounds__(kCtaThreads, 2) k_verify_sigw(StepParams P) {
             }
             mode = __shfl_sync(kFull, mode, 0);
             row = __shfl_sync(kFull, row, 0);
+            cur_b = b;
+            cur_mode = mode;
+            cur_row = row;
         }
+        issue((stage + kSigWStages - 1) % kSigWStages);
         cp_async_wait<kSigWStages - 1>();  // this thread's vectors of unit k have landed
         const int g0 = jw * GU;
         double2* out = P.gpart + (size_t)b * P.NG;
@@ -1949,27 +1958,13 @@ __global__ void __launch_bounds__(kCtaThreads, 2) k_verify_sigw(StepParams P) {
                 for (int h = 0; h < GU; ++h)
                     if (g0 + h < P.NG) st_slot(&out[g0 + h], make_double2(0.0, acc[h]));
             }
-        } else {
-            Decision d{};
-            d.mode = mode;
-            d.row = row;
-            d.Sp = d.Sq = 1.0;
-            // (rare at the sigmoid's acceptance) the pair from global, two
-            // granules' loads in flight at a time
-            for (int h = 0; h < GU; h += 2) {
-                GranuleData<T> D[2];
+        } else if (mode == MODE_NONE) {  // nothing to sample: the slots only flag completion
+            if (lane == 0) {
 #pragma unroll
-                for (int q = 0; q < 2; ++q)
-                    if (mode == MODE_REJECT && g0 + h + q < P.NG) granule_load<T>(P, b, g0 + h + q, d, D[q]);
-#pragma unroll
-                for (int q = 0; q < 2; ++q) {
-                    if (g0 + h + q >= P.NG) break;
-                    double2 gv = make_double2(0.0, 0.0);
-                    if (mode == MODE_REJECT) gv = granule_reduce<T, ACT>(P, d, D[q]);
-                    if (lane == 0) st_slot(&out[g0 + h + q], gv);
-                }
+                for (int h = 0; h < GU; ++h)
+                    if (g0 + h < P.NG) st_slot(&out[g0 + h], make_double2(0.0, 0.0));
             }
-        }
+        }  // MODE_REJECT: the reject phase below
         if (jw == 0 && lane == 0) trace(P, 8 * b + 3);
         stage = stage + 1 == kSigWStages ? 0 : stage + 1;
         if (++jw == NTW) {
@@ -1979,9 +1974,49 @@ __global__ void __launch_bounds__(kCtaThreads, 2) k_verify_sigw(StepParams P) {
     }
     cp_async_wait<0>();
     if (P.trace && P.sl_dbg && lane == 0) P.trace[8 * P.B + 26 + gw] = gtime();  // experiment: warp loop end
+    // 3. rejected rows (rare at the sigmoid's acceptance): their pair granules,
+    // spread over every warp of the grid once all decisions are in, two
+    // granules' loads in flight per warp (a rejected row reduced only by the
+    // warps that own its units made them stragglers: +15 us at B=256 V=32000).
+    if (tid == 0) {
+        while (ld_acquire(P.dec_cnt) < (unsigned)P.B) __nanosleep(64);
+        sh.last = (int)ld_acquire(P.rej_cnt);
+    }
+    __syncthreads();
+    const int R = sh.last;
+    for (int i = gw; i < R * NTW; i += nwarps) {
+        const int rb = __ldcg(&P.rej_list[i / NTW]), jr = i % NTW, g0 = jr * GU;
+        Decision d{};
+        d.mode = MODE_REJECT;
+        int rr = 0;
+        if (lane == 0) rr = wait_decision(P, rb).row;
+        d.row = __shfl_sync(kFull, rr, 0);
+        d.Sp = d.Sq = 1.0;
+        double2* out = P.gpart + (size_t)rb * P.NG;
+        for (int h = 0; h < GU; h += 2) {
+            GranuleData<T> D[2];
+#pragma unroll
+            for (int q = 0; q < 2; ++q)
+                if (g0 + h + q < P.NG) granule_load<T>(P, rb, g0 + h + q, d, D[q]);
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+                if (g0 + h + q >= P.NG) break;
+                const double2 gv = granule_reduce<T, ACT>(P, d, D[q]);
+                if (lane == 0) st_slot(&out[g0 + h + q], gv);
+            }
+        }
+    }
     __syncthreads();
     for (int b = grid - 1 - c; b < P.B; b += grid) locate_row<T, ACT>(P, b, sh, gcache);
-    if (P.trace && tid == 0) atomicMax(&P.trace[8 * P.B + 1], gtime());
+    if (tid == 0) {
+        if (P.trace) atomicMax(&P.trace[8 * P.B + 1], gtime());
+        __threadfence();
+        if (atomicAdd(P.exit_cnt, 1u) == gridDim.x - 1) {  // the last CTA out resets the counters
+            *P.rej_cnt = 0;
+            *P.dec_cnt = 0;
+            *P.exit_cnt = 0;
+        }
+    }
 }
 
 // ---------------------------------------------------------------------------

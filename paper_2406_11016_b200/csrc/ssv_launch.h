@@ -115,6 +115,9 @@ struct StepParams {
     double2* cgpart;   // [B][NG]    cluster path: granule partials (last-positive fallback)
     unsigned* next;     // [1] item claim counter   (reset by the last CTA to exit)
     unsigned* exit_cnt; // [1] CTAs done            (reset by the last CTA to exit)
+    unsigned* rej_cnt;  // [1] k_verify_sigw: rejected rows listed (reset by the last CTA to exit)
+    unsigned* dec_cnt;  // [1] k_verify_sigw: decisions made      (reset by the last CTA to exit)
+    int* rej_list;      // [B] k_verify_sigw: the rejected rows
     // outputs
     int32_t* acc;
     int32_t* fin;
