@@ -1838,6 +1838,29 @@ __global__ void __launch_bounds__(kCtaThreads, 2) k_verify_sig(StepParams P) {
 // reads only its own vectors through a kSigWStages-deep ring (the A-item
 // scheme), and lane 0 of each warp polls the decisions of its
 // next units.  Decisions first and the inverse CDFs last, as k_verify_sig.
+// Warp reduce-scatter of GU (2 or 4) per-lane partials: the first log2(GU)
+// butterfly levels exchange only the half each lane does not keep, so lane l
+// ends with the warp sum of value l / (32 / GU) after 5 (GU = 2) or 6 (GU = 4)
+// shuffles instead of 5 GU.
+template <int GU>
+__device__ __forceinline__ double warp_reduce_scatter(const double (&acc)[GU], int lane) {
+    static_assert(GU == 2 || GU == 4, "two or four values per lane");
+    double keep;
+    if constexpr (GU == 2) {
+        const bool up = lane & 16;
+        keep = (up ? acc[1] : acc[0]) + __shfl_xor_sync(kFull, up ? acc[0] : acc[1], 16);
+    } else {
+        const bool up = lane & 16;
+        const double k0 = (up ? acc[2] : acc[0]) + __shfl_xor_sync(kFull, up ? acc[0] : acc[2], 16);
+        const double k1 = (up ? acc[3] : acc[1]) + __shfl_xor_sync(kFull, up ? acc[1] : acc[3], 16);
+        const bool up8 = lane & 8;
+        keep = (up8 ? k1 : k0) + __shfl_xor_sync(kFull, up8 ? k0 : k1, 8);
+    }
+#pragma unroll
+    for (int o = 32 / GU / 2; o > 0; o >>= 1) keep += __shfl_xor_sync(kFull, keep, o);
+    return keep;
+}
+
 constexpr int kSigWNJ = 8;      // vectors per lane per unit
 constexpr int kSigWStages = 3;  // ring depth (2 units in flight per warp)
 constexpr int kSigWUnitVec = 32 * kSigWNJ;
@@ -1949,15 +1972,10 @@ __global__ void __launch_bounds__(kCtaThreads, 2) k_verify_sigw(StepParams P) {
                 }
                 acc[h] = a;
             }
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1)
-#pragma unroll
-                for (int h = 0; h < GU; ++h) acc[h] += __shfl_xor_sync(kFull, acc[h], o);
-            if (lane == 0) {
-#pragma unroll
-                for (int h = 0; h < GU; ++h)
-                    if (g0 + h < P.NG) st_slot(&out[g0 + h], make_double2(0.0, acc[h]));
-            }
+            // reduce-scatter: lane l ends with granule l / (32 / GU)'s sum (half the shuffles)
+            const double gs = warp_reduce_scatter<GU>(acc, lane);
+            const int hh = lane / (32 / GU);
+            if (lane % (32 / GU) == 0 && g0 + hh < P.NG) st_slot(&out[g0 + hh], make_double2(0.0, gs));
         } else if (mode == MODE_NONE) {  // nothing to sample: the slots only flag completion
             if (lane == 0) {
 #pragma unroll
