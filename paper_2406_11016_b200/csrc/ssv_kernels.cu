@@ -1881,7 +1881,21 @@ __global__ void __launch_bounds__(kCtaThreads, 2) k_verify_sigw(StepParams P) {
     const int nwarps = grid * kWarps, gw = c * kWarps + warp;
     // Each warp takes a contiguous range of units (one or two rows): the
     // decision changes only at a row boundary, and no division per unit.
-    const int u0 = (int)((long)gw * NU / nwarps), u1 = (int)((long)(gw + 1) * NU / nwarps);
+    // A warp that computes a decision first (phase 1: row b on warp (b / grid)
+    // % 8 of CTA b % grid) starts streaming ~5 us late, so its range is
+    // shorter: weight sg_dw / 16 against 16 / 16 (the deciding warps had been
+    // the last to finish at C4).  pos(w) = weighted warps before warp w.
+    // CTA c decides on min(8, ceil((B - c) / grid)) warps: with B = q grid + r,
+    // min(8, q + 1) for c < r and min(8, q) after (closed form, no loop).
+    const int dq = P.B / grid, dr = P.B - dq * grid, dhi = min(kWarps, dq + 1), dlo = min(kWarps, dq);
+    auto ndec_before = [&](int w) -> long {  // deciding warps among warps [0, w)
+        const int cw = w / kWarps, ww = w - cw * kWarps;
+        return (long)min(cw, dr) * dhi + (long)max(0, cw - dr) * dlo + min(ww, cw < dr ? dhi : dlo);
+    };
+    const int dw = P.sg_dw;
+    auto pos = [&](int w) -> long { return 16L * w - (16 - dw) * ndec_before(w); };
+    const long tot = pos(nwarps);
+    const int u0 = (int)(pos(gw) * NU / tot), u1 = (int)(pos(gw + 1) * NU / tot);
     const int nsteps = u1 - u0;
     const int nvec_row = (P.V + VEC - 1) / VEC;
     uint4* ring = reinterpret_cast<uint4*>(sigw_smem);  // [stage][j][thread]
@@ -3222,6 +3236,7 @@ static bool plan_sig_t(StepParams& P) {
     P.sg_on = 0;
     if (P.sample_mode) return false;
     static const int te_kb = knob("SSV_SIG_TE_KB", 48);  // 48 KB tiles: 32 KB 55 us, 64 KB (one CTA per SM) 67 us at C4
+    static const int sg_dw_env = knob("SSV_SIGW_DW16", 0);  // deciding warps' share (16ths); 0: by the stream length
     const int TE = te_kb * 1024 / (int)sizeof(T) / (kGW * kWarps) * (kGW * kWarps);  // multiple of kGW * kWarps
     const int tb = ((TE + 2 * (16 / (int)sizeof(T))) * (int)sizeof(T) + 127) & ~127;
     // Two CTAs per SM (16 warps to hide the per-element MUFU chains), each a
@@ -3257,6 +3272,11 @@ static bool plan_sig_t(StepParams& P) {
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pw, k_verify_sigw<T, ACT>, kCtaThreads, smemw);
             if (pw >= 1) {
                 P.sg_warp = 1;
+                // A decision costs a warp ~5 us of the stream (B * V * s bytes at ~6 TB/s):
+                // C4 43.7 -> 43.0 us at 13/16; B = 1024 loses 4 us at a fixed 13/16.
+                const double t_us = (double)P.B * P.V * sizeof(T) / 6.0e6;
+                const int dw = sg_dw_env > 0 ? sg_dw_env : (int)lround(16.0 * std::max(0.0, 1.0 - 5.0 / t_us));
+                P.sg_dw = std::max(1, std::min(16, dw));
                 P.sg_smem = smemw;
                 P.sg_grid = sm_count() * pw;
                 P.sg_te = TE;

@@ -88,6 +88,7 @@ struct StepParams {
     // tile buffers of sg_tb bytes per CTA.
     int sg_on, sg_te, sg_nt, sg_nbuf, sg_tb, sg_smem, sg_grid;
     int sg_warp;  // 1: k_verify_sigw (16-byte-aligned rows, barrier-free warp units)
+    int sg_dw;    // k_verify_sigw: a deciding warp's share of the stream, in 16ths of the others'
     // Optional grids written by the verify kernel itself (resident cluster plan:
     // every row slice is still in shared memory after the decision), else by
     // k_materialize as a second pass.
