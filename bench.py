@@ -145,7 +145,9 @@ def config_dict(key, variant, world):
     """The config both arms print (identical keys and values)."""
     desc, B, gamma, V, storage = WORKLOADS[key]
     return {"workload": desc, "variant": variant, "global_batch": B, "gamma": gamma, "V": V, "storage": storage,
-            "seed": SEED, "parallelism": f"batch rows sharded over {world} GPU(s) (strong scaling), no collective"}
+            "seed": SEED, "parallelism": f"batch rows sharded over {world} GPU(s) (strong scaling), no collective",
+            "l2": "inputs larger than L2: the device arm rotates input copies totalling > 3x L2 (details.l2), "
+                  "so every timed step reads its logits from HBM"}
 
 
 def algorithmic_bytes(variant, B, gamma, V, s, accepted_len):
